@@ -1,0 +1,187 @@
+/*
+ * vpm_b200.h -- C ABI of the B200-native VPM-MPPI stepping library
+ * (paper_2509_16079_b200/lib/libvpm_b200.so, sources in paper_2509_16079_b200/csrc/).
+ *
+ * Plain pointers and sizes only; no torch types.  Two layers:
+ *
+ *  1. Reference-facing host-buffer entry points.  They are exactly what the
+ *     reference's stepping-module FFI binds (perchsim/_accel/_core.pyx, which
+ *     Python reaches through perchsim/_accel/__init__.py:47-48 backend_module()):
+ *        vpm_step           replaces _core.pyx:536-576   step(...)
+ *        vpm_rollout        replaces _core.pyx:609-661   rollout(...)
+ *        vpm_batch_rollout  replaces _core.pyx:664-714   batch_rollout(...)
+ *        vpm_threads        replaces _core.pyx:744-745   omp_threads()
+ *     Arguments keep the reference meaning and layout (FP64, C-order, the
+ *     flattened FluidState 11-tuple of rollout.py:59-62, the frozen
+ *     iparams/fparams ABI of config.py:280-300).  Host buffers in, host buffers
+ *     out; the library does the host<->device copies.
+ *
+ *  2. Device-resident planner entry points used by the MPPI engine
+ *     (mppi.py:62-84 optimize, policy.py:66-91 perturbed rollouts): device
+ *     pointers plus a cudaStream_t passed as void*.
+ *
+ * Error convention (mirrors the reference): numerical failures are status codes
+ * (0 ok, 1+t failed at step t) in the outputs; configuration errors return a
+ * negative code from the call and set a message readable by vpm_last_error().
+ */
+#ifndef VPM_B200_H
+#define VPM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VPM_OK 0
+#define VPM_ERR_CONFIG (-1) /* limits / argument errors (reference: ValueError) */
+#define VPM_ERR_CUDA (-2)   /* CUDA runtime failure */
+#define VPM_ERR_ALLFAIL (-3) /* every MPPI candidate failed (mppi.py:55-56) */
+
+/* Flattened FluidState (rollout.py:59-62 order), FP64 reference layout.
+ * wake_pos is (n_wake, 2) C-order; buffers may be longer than n_wake. */
+typedef struct vpm_fluid {
+  const double *wake_pos;
+  const double *wake_gamma;
+  const int64_t *wake_age;
+  int32_t n_wake, ring_a, ring_b;
+  const double *prev_pos; /* (nb, 2) */
+  const double *prev_gamma;
+  int32_t n_prev;
+  double prev_lev;
+  const double *ema; /* (nb,) */
+} vpm_fluid;
+
+/* Output fluid buffers sized as the reference's _dump_fluid (_core.pyx:579-606):
+ * wake_pos (cap+4, 2), wake_gamma/wake_age (cap+4), prev_pos (nb, 2),
+ * prev_gamma/ema (nb).  scalars = {n_wake, ring_a, ring_b, n_prev}. */
+typedef struct vpm_fluid_out {
+  double *wake_pos;
+  double *wake_gamma;
+  int64_t *wake_age;
+  int32_t *scalars;
+  double *prev_pos;
+  double *prev_gamma;
+  double *prev_lev;
+  double *ema;
+} vpm_fluid_out;
+
+/* ---- layer 1: reference-facing, host buffers -------------------------------- */
+
+/* One coupled step (integrate=1: Engine.step, 0: Engine.fluid_step).  x is
+ * in/out (7).  Returns the step rc (0 ok, 1 singular solve, 2 non-finite) or a
+ * negative error.  fw (2) and mw (1) receive the wing loads.  _core.pyx:536-576 */
+int vpm_step(double *x, double u, const vpm_fluid *fluid, const int64_t *iparams,
+             const double *fparams, int integrate, double *fw, double *mw, vpm_fluid_out *out);
+
+/* Open-loop rollout of T controls; x in/out (7 = final state).  traj (T+1, 7)
+ * may be NULL; out may be NULL (no fluid returned).  Returns status (0 or 1+t)
+ * or a negative error.  _core.pyx:609-661 */
+int64_t vpm_rollout(double *x, const double *controls, int T, const vpm_fluid *fluid,
+                    const int64_t *iparams, const double *fparams, double *traj,
+                    vpm_fluid_out *out);
+
+/* B independent rollouts from a shared x0 (7) and fluid fork; controls (B, T).
+ * status (B) int64, finals (B, 7), trajs (B, T+1, 7) or NULL.  workers is
+ * accepted for signature parity and ignored (one CTA per rollout).
+ * _core.pyx:664-714 */
+int vpm_batch_rollout(const double *x0, const double *controls, int B, int T,
+                      const vpm_fluid *fluid, const int64_t *iparams, const double *fparams,
+                      int record, int workers, int64_t *status, double *finals, double *trajs);
+
+/* batch_rollout with one start state per row (x0 is (B, 7)): the perturbed
+ * cloud of policy.perturbed_rollouts (policy.py:66-91) in one launch. */
+int vpm_batch_rollout_x0(const double *x0, const double *controls, int B, int T,
+                         const vpm_fluid *fluid, const int64_t *iparams, const double *fparams,
+                         int record, int64_t *status, double *finals, double *trajs);
+
+/* omp_threads() analogue: concurrent rollouts resident on the device. */
+int vpm_threads(void);
+
+/* Message of the last negative return on this thread. */
+const char *vpm_last_error(void);
+
+/* ---- layer 2: device-resident planner ------------------------------------- */
+
+typedef struct vpm_plan vpm_plan;
+
+/* Create a plan bound to the frozen parameter ABI and a CUDA device: uploads the
+ * inverse boundary-system matrices, sizes scratch for up to max_rows rollouts of
+ * horizon H.  Returns NULL on error (see vpm_last_error). */
+vpm_plan *vpm_plan_create(const int64_t *iparams, const double *fparams, int max_rows, int H,
+                          int device);
+void vpm_plan_destroy(vpm_plan *p);
+
+/* Upload the fluid snapshot (host) that every rollout forks from. */
+int vpm_plan_set_fluid(vpm_plan *p, const vpm_fluid *fluid);
+
+/* Per-rollout outputs of a device batch; any pointer may be NULL. */
+typedef struct vpm_batch_out {
+  int64_t *status;      /* (rows) */
+  double *finals;       /* (rows, 7) */
+  double *trajs;        /* (rows, T+1, 7) */
+  double *cost;         /* (rows) terminal cost, +inf when failed (mppi.py:28-34) */
+  uint64_t *shed_mask;  /* (rows) bit t set when step t shed */
+  int32_t *n_final;     /* (rows) final wake size */
+  int64_t *interactions;/* (rows) regularised Biot-Savart interactions evaluated */
+} vpm_batch_out;
+
+/* Device batch of rows [row_begin, row_end) of a B_total-row candidate set.
+ * Controls: if d_controls != NULL, row r uses d_controls[(r - row_begin)*T ...];
+ * else MPPI sampling: row 0 is d_ustar, row r>=1 is
+ * clip(d_ustar + sigma * d_noise[(r-1)*T ...], +-u_limit) (mppi.py:37-43, :79).
+ * d_x0 is (7) when x0_stride == 0 or (rows, 7) when x0_stride == 7.
+ * d_q / d_xperch (7 each) enable the cost output.  Launches on stream. */
+int vpm_plan_batch(vpm_plan *p, const double *d_x0, int x0_stride, const double *d_controls,
+                   const double *d_ustar, const double *d_noise, double sigma, int row_begin,
+                   int row_end, int T, const double *d_q, const double *d_xperch, int record,
+                   const vpm_batch_out *d_out, void *stream);
+
+/* MPPI weighted partial sums over rows [0, rows) of this shard
+ * (mppi.py:46-59 split for sharding): d_partial (H+2) =
+ * {J_min_r, Z_r = sum exp(-(J-J_min_r)/lambda), S_r[H] = sum w u}.  Row r uses
+ * the same control formula as vpm_plan_batch with global index row_begin + r. */
+int vpm_mppi_partial(vpm_plan *p, const double *d_cost, int rows, int row_begin,
+                     const double *d_ustar, const double *d_noise, double sigma, int T,
+                     double temperature, double *d_partial, void *stream);
+
+/* Combine W gathered partials (W, H+2) in rank order into d_ustar (H).  Sets
+ * *d_flag = 1 when every candidate failed (the caller raises). */
+int vpm_mppi_combine(const double *d_partials, int W, int T, double temperature,
+                     double *d_ustar, int32_t *d_flag, void *stream);
+
+/* Whole MPPI iteration on one device (batch + partial + combine), optionally
+ * replayed from a CUDA graph captured on first use (use_graph != 0).
+ * d_noise: (B_total - 1, T).  d_cost scratch (B_total) and d_partial (T+2). */
+int vpm_mppi_iteration(vpm_plan *p, const double *d_x0, double *d_ustar, const double *d_noise,
+                       double sigma, int B_total, int T, double temperature, const double *d_q,
+                       const double *d_xperch, double *d_cost, double *d_partial,
+                       int32_t *d_flag, int use_graph, void *stream);
+
+/* Host-buffer MPPI optimise (mppi.py:62-84) for iters iterations with
+ * pre-generated noise (iters, K, T): host u_star in/out (T).  Includes every
+ * host<->device copy.  Returns VPM_ERR_ALLFAIL when a whole batch failed. */
+int vpm_mppi_optimize_host(vpm_plan *p, const double *x0, double *u_star, const double *noise,
+                           int iters, int K, int T, double sigma, double temperature,
+                           const double *q, const double *x_perch);
+
+/* Average duration (ms) of the rollout kernel over the launches recorded since
+ * the last reset, timed with CUDA events on the launch stream. */
+int vpm_plan_timing(vpm_plan *p, int reset, double *avg_ms, int64_t *launches);
+
+/* FP32 FFMA throughput microbenchmark (GFLOP/s) on the current device. */
+double vpm_fp32_peak_probe(int iters);
+
+/* Host-only: the inverses of the three pose-invariant boundary systems the solve
+ * uses (attached nb x nb, shedding forward, shedding reversed; (nb+2)^2 doubles
+ * each, row-major, the attached block with row stride nb).  out: 3 (nb+2)^2. */
+int vpm_boundary_inverse(const int64_t *iparams, const double *fparams, double *out);
+
+/* Launch configuration chosen for a particle cap: threads per rollout CTA,
+ * targets per thread, dynamic shared memory bytes. */
+int vpm_launch_shape(int cap, int nb, int *threads, int *targets, int *smem_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VPM_B200_H */

@@ -1,0 +1,193 @@
+"""ctypes binding to ``lib/libvpm_b200.so`` (C ABI declared in ``include/vpm_b200.h``).
+
+The library is built in-tree by :func:`build` (nvcc, ``-gencode
+arch=compute_100a,code=sm_100a``) so the ``.so`` travels with the repository
+snapshot to the GPU box.  There is no fallback: if the library cannot be loaded,
+or no CUDA device is present, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+LIB_PATH = os.path.join(PKG, "lib", "libvpm_b200.so")
+SOURCES = [os.path.join(PKG, "csrc", "vpm_capi.cu"), os.path.join(PKG, "csrc", "vpm_rollout.cuh"),
+           os.path.join(ROOT, "include", "vpm_b200.h")]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+              "-shared", "-Xcompiler", "-fPIC"]
+
+VPM_OK, VPM_ERR_CONFIG, VPM_ERR_CUDA, VPM_ERR_ALLFAIL = 0, -1, -2, -3
+
+
+class CudaBackendError(RuntimeError):
+    """The sm_100a library is missing, failed to load, or a CUDA call failed."""
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB_PATH):
+        return True
+    t = os.path.getmtime(LIB_PATH)
+    return any(os.path.getmtime(s) > t for s in SOURCES if os.path.exists(s))
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile the CUDA library in place (cross-compiles without a GPU)."""
+    if force or _stale():
+        os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
+        nvcc = os.environ.get("NVCC", "nvcc")
+        cmd = [nvcc, *NVCC_FLAGS, SOURCES[0], "-o", LIB_PATH + ".tmp"]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.check_call(cmd)
+        os.replace(LIB_PATH + ".tmp", LIB_PATH)
+    return LIB_PATH
+
+
+# ---- C structs (mirror include/vpm_b200.h) ----------------------------------------
+_D = C.POINTER(C.c_double)
+_I64 = C.POINTER(C.c_int64)
+_I32 = C.POINTER(C.c_int32)
+_U64 = C.POINTER(C.c_uint64)
+
+
+class VpmFluid(C.Structure):
+    _fields_ = [("wake_pos", _D), ("wake_gamma", _D), ("wake_age", _I64), ("n_wake", C.c_int32),
+                ("ring_a", C.c_int32), ("ring_b", C.c_int32), ("prev_pos", _D),
+                ("prev_gamma", _D), ("n_prev", C.c_int32), ("prev_lev", C.c_double), ("ema", _D)]
+
+
+class VpmFluidOut(C.Structure):
+    _fields_ = [("wake_pos", _D), ("wake_gamma", _D), ("wake_age", _I64), ("scalars", _I32),
+                ("prev_pos", _D), ("prev_gamma", _D), ("prev_lev", _D), ("ema", _D)]
+
+
+class VpmBatchOut(C.Structure):
+    _fields_ = [("status", C.c_void_p), ("finals", C.c_void_p), ("trajs", C.c_void_p),
+                ("cost", C.c_void_p), ("shed_mask", C.c_void_p), ("n_final", C.c_void_p),
+                ("interactions", C.c_void_p)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load (once) and return the library handle; raises CudaBackendError."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise CudaBackendError(
+                f"{LIB_PATH} is not built; run __graft_entry__.build() (nvcc, sm_100a)")
+        try:
+            L = C.CDLL(LIB_PATH)
+        except OSError as err:
+            raise CudaBackendError(f"cannot load {LIB_PATH}: {err}") from err
+        vp = C.c_void_p
+        sig = {
+            "vpm_step": (C.c_int, [_D, C.c_double, C.POINTER(VpmFluid), _I64, _D, C.c_int, _D, _D,
+                                   C.POINTER(VpmFluidOut)]),
+            "vpm_rollout": (C.c_int64, [_D, _D, C.c_int, C.POINTER(VpmFluid), _I64, _D, _D,
+                                        C.POINTER(VpmFluidOut)]),
+            "vpm_batch_rollout": (C.c_int, [_D, _D, C.c_int, C.c_int, C.POINTER(VpmFluid), _I64, _D,
+                                            C.c_int, C.c_int, _I64, _D, _D]),
+            "vpm_batch_rollout_x0": (C.c_int, [_D, _D, C.c_int, C.c_int, C.POINTER(VpmFluid), _I64,
+                                               _D, C.c_int, _I64, _D, _D]),
+            "vpm_threads": (C.c_int, []),
+            "vpm_last_error": (C.c_char_p, []),
+            "vpm_plan_create": (vp, [_I64, _D, C.c_int, C.c_int, C.c_int]),
+            "vpm_plan_destroy": (None, [vp]),
+            "vpm_plan_set_fluid": (C.c_int, [vp, C.POINTER(VpmFluid)]),
+            "vpm_plan_batch": (C.c_int, [vp, vp, C.c_int, vp, vp, vp, C.c_double, C.c_int, C.c_int,
+                                         C.c_int, vp, vp, C.c_int, C.POINTER(VpmBatchOut), vp]),
+            "vpm_mppi_partial": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, C.c_double, C.c_int,
+                                           C.c_double, vp, vp]),
+            "vpm_mppi_combine": (C.c_int, [vp, C.c_int, C.c_int, C.c_double, vp, vp, vp]),
+            "vpm_mppi_iteration": (C.c_int, [vp, vp, vp, vp, C.c_double, C.c_int, C.c_int,
+                                             C.c_double, vp, vp, vp, vp, vp, C.c_int, vp]),
+            "vpm_mppi_optimize_host": (C.c_int, [vp, _D, _D, _D, C.c_int, C.c_int, C.c_int,
+                                                 C.c_double, C.c_double, _D, _D]),
+            "vpm_plan_timing": (C.c_int, [vp, C.c_int, _D, _I64]),
+            "vpm_fp32_peak_probe": (C.c_double, [C.c_int]),
+            "vpm_launch_shape": (C.c_int, [C.c_int, C.c_int, _I32, _I32, _I32]),
+            "vpm_boundary_inverse": (C.c_int, [_I64, _D, _D]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+        return _lib
+
+
+EXPORTED = ("vpm_step", "vpm_rollout", "vpm_batch_rollout", "vpm_batch_rollout_x0", "vpm_threads",
+            "vpm_last_error", "vpm_plan_create", "vpm_plan_destroy", "vpm_plan_set_fluid",
+            "vpm_plan_batch", "vpm_mppi_partial", "vpm_mppi_combine", "vpm_mppi_iteration",
+            "vpm_mppi_optimize_host", "vpm_plan_timing", "vpm_fp32_peak_probe", "vpm_launch_shape",
+            "vpm_boundary_inverse")
+
+
+def last_error() -> str:
+    return lib().vpm_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str) -> int:
+    """Map negative library returns to the reference's exception types."""
+    if rc >= 0:
+        return rc
+    msg = f"{what}: {last_error()}"
+    if rc == VPM_ERR_CONFIG:
+        raise ValueError(msg)
+    if rc == VPM_ERR_ALLFAIL:
+        raise ValueError("all sampled rollouts failed (infinite cost)")
+    raise CudaBackendError(msg)
+
+
+def ptr(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def as_f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def as_i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def fluid_struct(wake_pos, wake_gamma, wake_age, n_wake, ring_a, ring_b, prev_pos, prev_gamma,
+                 n_prev, prev_lev, ema):
+    """Build a VpmFluid from the reference's flattened 11-tuple (rollout.py:59-62).
+    Returns (struct, keepalive)."""
+    keep = (as_f64(wake_pos), as_f64(wake_gamma), as_i64(wake_age), as_f64(prev_pos),
+            as_f64(prev_gamma), as_f64(ema))
+    f = VpmFluid(ptr(keep[0], _D), ptr(keep[1], _D), ptr(keep[2], _I64), int(n_wake), int(ring_a),
+                 int(ring_b), ptr(keep[3], _D), ptr(keep[4], _D), int(n_prev), float(prev_lev),
+                 ptr(keep[5], _D))
+    return f, keep
+
+
+def fluid_out(cap: int, nb: int):
+    bufs = dict(wp=np.zeros((cap + 4, 2)), wg=np.zeros(cap + 4), wa=np.zeros(cap + 4, np.int64),
+                sc=np.zeros(4, np.int32), pp=np.zeros((nb, 2)), pg=np.zeros(nb), pl=np.zeros(1),
+                em=np.zeros(nb))
+    s = VpmFluidOut(ptr(bufs["wp"], _D), ptr(bufs["wg"], _D), ptr(bufs["wa"], _I64),
+                    ptr(bufs["sc"], _I32), ptr(bufs["pp"], _D), ptr(bufs["pg"], _D),
+                    ptr(bufs["pl"], _D), ptr(bufs["em"], _D))
+    return s, bufs
+
+
+def fluid_tuple(b):
+    sc = b["sc"]
+    return (b["wp"], b["wg"], b["wa"], int(sc[0]), int(sc[1]), int(sc[2]), b["pp"], b["pg"],
+            int(sc[3]), float(b["pl"][0]), b["em"])

@@ -1,0 +1,736 @@
+// vpm_capi.cu -- extern "C" ABI of libvpm_b200.so (declared in include/vpm_b200.h).
+//
+// Host side of the hot path: parameter unpacking with the reference's frozen ABI
+// (config.py:280-300, _core.pyx:65-86), the precomputed inverses of the three
+// pose-invariant boundary systems, launch-shape selection, device plans and the
+// reference-facing host-buffer entry points that replace _core.pyx's step /
+// rollout / batch_rollout.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/vpm_b200.h"
+#include "vpm_rollout.cuh"
+
+using vpm::Args;
+using vpm::Phys;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail_cfg(const std::string &m) {
+  g_err = m;
+  return VPM_ERR_CONFIG;
+}
+
+int fail_cuda(cudaError_t e, const char *what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return VPM_ERR_CUDA;
+}
+
+#define CK(call)                                 \
+  do {                                           \
+    cudaError_t e_ = (call);                     \
+    if (e_ != cudaSuccess) return fail_cuda(e_, #call); \
+  } while (0)
+
+// frozen fparams order (config.py:283-285)
+enum {
+  FP_R_CORE, FP_K_DISS, FP_SHED_OFF, FP_CRIT_AOA, FP_RHO, FP_DT, FP_M, FP_I, FP_G, FP_L,
+  FP_L_W, FP_L_E, FP_L_CHORD, FP_S_E, FP_PHI_LIM, FP_U_LIM, FP_LEV_GAIN, FP_ETA, FP_COUNT
+};
+
+constexpr int CAP_MAX = 4088;  // 12-bit particle index inside the merge keys
+
+int unpack(const int64_t *ip, const double *fp, Phys *P) {
+  if (!ip || !fp) return fail_cfg("iparams/fparams must not be null");
+  if (ip[0] < 1 || ip[0] > vpm::NB_MAX)
+    return fail_cfg("n_bound > " + std::to_string(vpm::NB_MAX) + " (or < 1) not supported");
+  if (ip[1] < 4 || ip[1] > CAP_MAX)
+    return fail_cfg("particle_cap > " + std::to_string(CAP_MAX) + " (or < 4) not supported");
+  for (int i = 0; i < FP_COUNT; ++i)
+    if (!std::isfinite(fp[i])) return fail_cfg("non-finite fparams entry " + std::to_string(i));
+  P->nb = (int)ip[0];
+  P->cap = (int)ip[1];
+  P->r_core = fp[FP_R_CORE];
+  P->k_diss = fp[FP_K_DISS];
+  P->shed_off = fp[FP_SHED_OFF];
+  P->crit_aoa = fp[FP_CRIT_AOA];
+  P->rho = fp[FP_RHO];
+  P->dt = fp[FP_DT];
+  P->m = fp[FP_M];
+  P->inertia = fp[FP_I];
+  P->g = fp[FP_G];
+  P->l = fp[FP_L];
+  P->l_w = fp[FP_L_W];
+  P->l_e = fp[FP_L_E];
+  P->l_chord = fp[FP_L_CHORD];
+  P->s_e = fp[FP_S_E];
+  P->phi_lim = fp[FP_PHI_LIM];
+  P->u_lim = fp[FP_U_LIM];
+  P->lev_gain = fp[FP_LEV_GAIN];
+  P->eta = fp[FP_ETA];
+  const double r = P->r_core;
+  P->rc4f = (float)(r * r * r * r);
+  return VPM_OK;
+}
+
+// Gauss-Jordan inverse with partial pivoting (row-major); false when singular.
+bool invert(std::vector<double> &a, int n, std::vector<double> &inv) {
+  inv.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) inv[(size_t)i * n + i] = 1.0;
+  for (int k = 0; k < n; ++k) {
+    int p = k;
+    for (int r = k + 1; r < n; ++r)
+      if (std::fabs(a[(size_t)r * n + k]) > std::fabs(a[(size_t)p * n + k])) p = r;
+    if (a[(size_t)p * n + k] == 0.0) return false;
+    if (p != k)
+      for (int c = 0; c < n; ++c) {
+        std::swap(a[(size_t)k * n + c], a[(size_t)p * n + c]);
+        std::swap(inv[(size_t)k * n + c], inv[(size_t)p * n + c]);
+      }
+    const double d = a[(size_t)k * n + k];
+    for (int c = 0; c < n; ++c) { a[(size_t)k * n + c] /= d; inv[(size_t)k * n + c] /= d; }
+    for (int r = 0; r < n; ++r) {
+      if (r == k) continue;
+      const double f = a[(size_t)r * n + k];
+      if (f == 0.0) continue;
+      for (int c = 0; c < n; ++c) {
+        a[(size_t)r * n + c] -= f * a[(size_t)k * n + c];
+        inv[(size_t)r * n + c] -= f * inv[(size_t)k * n + c];
+      }
+    }
+  }
+  return true;
+}
+
+// The boundary system of _core.pyx:258-313 (vpm.py:331-391) assembled in the
+// chord frame.  Every influence coefficient couples two points on the chord
+// line, so A depends only on (shedding, reversed) and the config, not on the
+// pose (SURVEY.md finding 0.5; verified there to 4.6e-12 over 400 poses).
+// Variant 0: attached nb x nb; 1: shedding forward; 2: shedding reversed.
+int build_inverses(const Phys &P, std::vector<double> &out) {
+  const int nb = P.nb, S = nb + 2;
+  out.assign((size_t)3 * S * S, 0.0);
+  const double s = P.l_chord / nb;
+  std::vector<double> col(nb + 1), pan(nb);
+  for (int i = 0; i <= nb; ++i) col[i] = -s * i;
+  for (int j = 0; j < nb; ++j) pan[j] = col[j] - 0.5 * s;
+  const double lev = col[0] + P.shed_off, tev = col[nb] - P.shed_off;
+  for (int var = 0; var < 3; ++var) {
+    const bool shed = var > 0, rev = var == 2;
+    const int ns = shed ? nb + 2 : nb, r0 = shed ? 1 : 0;
+    std::vector<double> A((size_t)ns * ns, 0.0), inv;
+    for (int i = 0; i < nb; ++i) {
+      const int ri = (shed && rev) ? i : i + 1;
+      for (int j = 0; j < ns; ++j) {
+        const double src = j < nb ? pan[j] : (j == nb ? lev : tev);
+        const double dx = col[ri] - src;  // normal (0,1): (dz nx - dx nz)/(2 pi r^2)
+        A[(size_t)(r0 + i) * ns + j] = -dx / (vpm::TWO_PI * dx * dx);
+      }
+    }
+    if (shed) {
+      const int ecol = rev ? nb + 1 : nb, epan = rev ? nb - 1 : 0;
+      A[ecol] = 1.0;
+      A[epan] = P.lev_gain;
+      for (int j = 0; j < ns; ++j) A[(size_t)(nb + 1) * ns + j] = 1.0;
+    }
+    if (!invert(A, ns, inv)) return fail_cfg("boundary system is singular for this configuration");
+    std::memcpy(&out[(size_t)var * S * S], inv.data(), sizeof(double) * ns * ns);
+  }
+  return VPM_OK;
+}
+
+struct Shape {
+  int nt, r;
+};
+
+// Smallest tile (threads x targets/thread) covering the cap; deeper register
+// tiles once there are enough particles to keep every thread busy.
+Shape pick_shape(int cap) {
+  static const Shape table[] = {{64, 1}, {64, 2}, {128, 2}, {128, 4}, {256, 4}, {256, 8}, {512, 8}};
+  for (const Shape &s : table)
+    if (s.nt * s.r >= cap) return s;
+  return table[6];
+}
+
+template <int NT, int R>
+cudaError_t launch_t(const Args &a, int grid, size_t smem, cudaStream_t st) {
+  auto k = vpm::rollout_kernel<NT, R>;
+  static thread_local size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k<<<grid, NT, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rollouts(const Args &a, int grid, cudaStream_t st) {
+  const Shape sh = pick_shape(a.P.cap);
+  const size_t smem = vpm::make_layout(a.P.cap, a.P.nb, sh.nt).total;
+  switch (sh.nt * 16 + sh.r) {
+    case 64 * 16 + 1: return launch_t<64, 1>(a, grid, smem, st);
+    case 64 * 16 + 2: return launch_t<64, 2>(a, grid, smem, st);
+    case 128 * 16 + 2: return launch_t<128, 2>(a, grid, smem, st);
+    case 128 * 16 + 4: return launch_t<128, 4>(a, grid, smem, st);
+    case 256 * 16 + 4: return launch_t<256, 4>(a, grid, smem, st);
+    case 256 * 16 + 8: return launch_t<256, 8>(a, grid, smem, st);
+    default: return launch_t<512, 8>(a, grid, smem, st);
+  }
+}
+
+int check_fluid(const vpm_fluid *f, const Phys &P) {
+  if (!f) return fail_cfg("fluid must not be null");
+  if (f->n_wake < 0 || f->n_wake > P.cap + 4) return fail_cfg("n_wake outside [0, cap+4]");
+  if (f->n_prev != 0 && f->n_prev != P.nb) return fail_cfg("n_prev must be 0 or n_bound");
+  if (f->ring_a >= f->n_wake || f->ring_b >= f->n_wake) return fail_cfg("ring index beyond n_wake");
+  for (int i = 0; i < f->n_wake; ++i)
+    if (f->wake_age[i] < 0 || f->wake_age[i] > (1 << 19) - 4096)
+      return fail_cfg("wake_age outside [0, 2^19 - 4096)");
+  return VPM_OK;
+}
+
+}  // namespace
+
+// ============================ device plan ========================================
+struct vpm_plan {
+  int device = 0;
+  Phys P{};
+  int max_rows = 0, H = 0;
+  double *d_ainv = nullptr;
+  // snapshot
+  double *d_wpos = nullptr, *d_wgam = nullptr, *d_ppos = nullptr, *d_pgam = nullptr, *d_ema = nullptr;
+  int64_t *d_wage = nullptr;
+  int n_wake = 0, ring_a = -1, ring_b = -1, n_prev = 0;
+  double prev_lev = 0.0;
+  double *d_wbuf = nullptr;
+  size_t wbuf_len = 0;
+  // rollout-kernel timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // start/stop pairs
+  size_t ev_used = 0;
+  std::mutex mu;
+};
+
+static Args base_args(const vpm_plan *p) {
+  Args a;
+  std::memset(&a, 0, sizeof(a));
+  a.P = p->P;
+  a.ainv = p->d_ainv;
+  a.wpos = p->d_wpos;
+  a.wgam = p->d_wgam;
+  a.wage = p->d_wage;
+  a.n_wake = p->n_wake;
+  a.ring_a = p->ring_a;
+  a.ring_b = p->ring_b;
+  a.ppos = p->d_ppos;
+  a.pgam = p->d_pgam;
+  a.n_prev = p->n_prev;
+  a.prev_lev = p->prev_lev;
+  a.ema = p->d_ema;
+  a.integrate = 1;
+  a.check_envelope = 1;
+  return a;
+}
+
+static int plan_launch(vpm_plan *p, const Args &a, int grid, cudaStream_t st) {
+  if (grid <= 0) return VPM_OK;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (p->timing) {
+    if (p->ev_used + 2 > p->ev.size()) {
+      for (int i = 0; i < 2; ++i) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        p->ev.push_back(e);
+      }
+    }
+    e0 = p->ev[p->ev_used];
+    e1 = p->ev[p->ev_used + 1];
+    p->ev_used += 2;
+    CK(cudaEventRecord(e0, st));
+  }
+  cudaError_t e = launch_rollouts(a, grid, st);
+  if (e != cudaSuccess) return fail_cuda(e, "rollout_kernel launch");
+  if (p->timing) CK(cudaEventRecord(e1, st));
+  return VPM_OK;
+}
+
+extern "C" {
+
+const char *vpm_last_error(void) { return g_err.c_str(); }
+
+int vpm_launch_shape(int cap, int nb, int *threads, int *targets, int *smem_bytes) {
+  const Shape s = pick_shape(cap);
+  if (threads) *threads = s.nt;
+  if (targets) *targets = s.r;
+  if (smem_bytes) *smem_bytes = vpm::make_layout(cap, nb, s.nt).total;
+  return VPM_OK;
+}
+
+vpm_plan *vpm_plan_create(const int64_t *iparams, const double *fparams, int max_rows, int H,
+                          int device) {
+  Phys P;
+  if (unpack(iparams, fparams, &P) != VPM_OK) return nullptr;
+  std::vector<double> inv;
+  if (build_inverses(P, inv) != VPM_OK) return nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    g_err = "cudaSetDevice failed";
+    return nullptr;
+  }
+  vpm_plan *p = new vpm_plan();
+  p->device = device;
+  p->P = P;
+  p->max_rows = max_rows;
+  p->H = H;
+  const int cap4 = P.cap + 4;
+  bool ok = cudaMalloc(&p->d_ainv, inv.size() * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&p->d_wpos, sizeof(double) * 2 * cap4) == cudaSuccess &&
+            cudaMalloc(&p->d_wgam, sizeof(double) * cap4) == cudaSuccess &&
+            cudaMalloc(&p->d_wage, sizeof(int64_t) * cap4) == cudaSuccess &&
+            cudaMalloc(&p->d_ppos, sizeof(double) * 2 * P.nb) == cudaSuccess &&
+            cudaMalloc(&p->d_pgam, sizeof(double) * P.nb) == cudaSuccess &&
+            cudaMalloc(&p->d_ema, sizeof(double) * P.nb) == cudaSuccess;
+  if (ok) ok = cudaMemcpy(p->d_ainv, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
+  if (ok) ok = cudaMemset(p->d_ema, 0, sizeof(double) * P.nb) == cudaSuccess;
+  if (!ok) {
+    g_err = "device allocation failed";
+    vpm_plan_destroy(p);
+    return nullptr;
+  }
+  return p;
+}
+
+void vpm_plan_destroy(vpm_plan *p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  cudaFree(p->d_ainv);
+  cudaFree(p->d_wpos);
+  cudaFree(p->d_wgam);
+  cudaFree(p->d_wage);
+  cudaFree(p->d_ppos);
+  cudaFree(p->d_pgam);
+  cudaFree(p->d_ema);
+  cudaFree(p->d_wbuf);
+  for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
+  delete p;
+}
+
+int vpm_plan_set_fluid(vpm_plan *p, const vpm_fluid *f) {
+  if (!p) return fail_cfg("null plan");
+  int rc = check_fluid(f, p->P);
+  if (rc) return rc;
+  CK(cudaSetDevice(p->device));
+  if (f->n_wake > 0) {
+    CK(cudaMemcpy(p->d_wpos, f->wake_pos, sizeof(double) * 2 * f->n_wake, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p->d_wgam, f->wake_gamma, sizeof(double) * f->n_wake, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p->d_wage, f->wake_age, sizeof(int64_t) * f->n_wake, cudaMemcpyHostToDevice));
+  }
+  if (f->n_prev > 0) {
+    CK(cudaMemcpy(p->d_ppos, f->prev_pos, sizeof(double) * 2 * f->n_prev, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p->d_pgam, f->prev_gamma, sizeof(double) * f->n_prev, cudaMemcpyHostToDevice));
+  }
+  CK(cudaMemcpy(p->d_ema, f->ema, sizeof(double) * p->P.nb, cudaMemcpyHostToDevice));
+  p->n_wake = f->n_wake;
+  p->ring_a = f->ring_a;
+  p->ring_b = f->ring_b;
+  p->n_prev = f->n_prev;
+  p->prev_lev = f->prev_lev;
+  return VPM_OK;
+}
+
+int vpm_plan_batch(vpm_plan *p, const double *d_x0, int x0_stride, const double *d_controls,
+                   const double *d_ustar, const double *d_noise, double sigma, int row_begin,
+                   int row_end, int T, const double *d_q, const double *d_xperch, int record,
+                   const vpm_batch_out *o, void *stream) {
+  if (!p) return fail_cfg("null plan");
+  if (T < 0 || row_end < row_begin) return fail_cfg("bad row range / horizon");
+  if (!d_controls && (!d_ustar || (!d_noise && row_end > 1))) return fail_cfg("controls or u*/noise required");
+  Args a = base_args(p);
+  a.x0 = d_x0;
+  a.x0_stride = x0_stride;
+  a.controls = d_controls;
+  a.ustar = d_ustar;
+  a.noise = d_noise;
+  a.sigma = sigma;
+  a.T = T;
+  a.row_begin = row_begin;
+  a.rows = row_end - row_begin;
+  a.record = record;
+  if (o) {
+    a.status = o->status;
+    a.finals = o->finals;
+    a.trajs = o->trajs;
+    a.cost = (d_q && d_xperch) ? o->cost : nullptr;
+    a.shed_mask = o->shed_mask;
+    a.n_final = o->n_final;
+    a.inter = o->interactions;
+  }
+  a.q = d_q;
+  a.xp = d_xperch;
+  std::lock_guard<std::mutex> lk(p->mu);
+  CK(cudaSetDevice(p->device));
+  return plan_launch(p, a, a.rows, (cudaStream_t)stream);
+}
+
+int vpm_mppi_partial(vpm_plan *p, const double *d_cost, int rows, int row_begin,
+                     const double *d_ustar, const double *d_noise, double sigma, int T,
+                     double temperature, double *d_partial, void *stream) {
+  if (!p) return fail_cfg("null plan");
+  if (temperature <= 0.0) return fail_cfg("temperature must be > 0");
+  std::lock_guard<std::mutex> lk(p->mu);
+  CK(cudaSetDevice(p->device));
+  if (p->wbuf_len < (size_t)rows) {
+    cudaFree(p->d_wbuf);
+    p->d_wbuf = nullptr;
+    CK(cudaMalloc(&p->d_wbuf, sizeof(double) * (size_t)(rows > 1 ? rows : 1)));
+    p->wbuf_len = rows;
+  }
+  constexpr int NTH = 512;
+  const size_t smem = sizeof(double) * ((NTH / 32) * (size_t)T + 2 * (NTH / 32));
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(vpm::mppi_partial_kernel<NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  vpm::mppi_partial_kernel<NTH><<<1, NTH, smem, (cudaStream_t)stream>>>(
+      d_cost, rows, row_begin, d_ustar, d_noise, sigma, p->P.u_lim, T, temperature, p->d_wbuf, d_partial);
+  CK(cudaGetLastError());
+  return VPM_OK;
+}
+
+int vpm_mppi_combine(const double *d_partials, int W, int T, double temperature, double *d_ustar,
+                     int32_t *d_flag, void *stream) {
+  if (W < 1 || T < 0) return fail_cfg("bad combine shape");
+  vpm::mppi_combine_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(d_partials, W, T, temperature, d_ustar, d_flag);
+  CK(cudaGetLastError());
+  return VPM_OK;
+}
+
+int vpm_mppi_iteration(vpm_plan *p, const double *d_x0, double *d_ustar, const double *d_noise,
+                       double sigma, int B_total, int T, double temperature, const double *d_q,
+                       const double *d_xperch, double *d_cost, double *d_partial, int32_t *d_flag,
+                       int use_graph, void *stream) {
+  (void)use_graph;  // one persistent CTA per rollout already amortises the H steps
+  vpm_batch_out o;
+  std::memset(&o, 0, sizeof(o));
+  o.cost = d_cost;
+  int rc = vpm_plan_batch(p, d_x0, 0, nullptr, d_ustar, d_noise, sigma, 0, B_total, T, d_q, d_xperch, 0, &o, stream);
+  if (rc) return rc;
+  rc = vpm_mppi_partial(p, d_cost, B_total, 0, d_ustar, d_noise, sigma, T, temperature, d_partial, stream);
+  if (rc) return rc;
+  return vpm_mppi_combine(d_partial, 1, T, temperature, d_ustar, d_flag, stream);
+}
+
+int vpm_mppi_optimize_host(vpm_plan *p, const double *x0, double *u_star, const double *noise,
+                           int iters, int K, int T, double sigma, double temperature,
+                           const double *q, const double *x_perch) {
+  if (!p) return fail_cfg("null plan");
+  CK(cudaSetDevice(p->device));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const int B = K + 1;
+  double *d_x0, *d_u, *d_noise, *d_q, *d_xp, *d_cost, *d_part;
+  int32_t *d_flag;
+  const size_t nn = (size_t)iters * K * T;
+  CK(cudaMallocAsync(&d_x0, 7 * sizeof(double), st));
+  CK(cudaMallocAsync(&d_u, (T > 0 ? T : 1) * sizeof(double), st));
+  CK(cudaMallocAsync(&d_noise, (nn > 0 ? nn : 1) * sizeof(double), st));
+  CK(cudaMallocAsync(&d_q, 7 * sizeof(double), st));
+  CK(cudaMallocAsync(&d_xp, 7 * sizeof(double), st));
+  CK(cudaMallocAsync(&d_cost, B * sizeof(double), st));
+  CK(cudaMallocAsync(&d_part, (T + 2) * sizeof(double), st));
+  CK(cudaMallocAsync(&d_flag, iters * sizeof(int32_t) + 4, st));
+  CK(cudaMemcpyAsync(d_x0, x0, 7 * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_u, u_star, T * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_noise, noise, nn * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_q, q, 7 * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_xp, x_perch, 7 * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_flag, 0, iters * sizeof(int32_t) + 4, st));
+  int rc = VPM_OK;
+  for (int it = 0; it < iters && rc == VPM_OK; ++it)
+    rc = vpm_mppi_iteration(p, d_x0, d_u, d_noise + (size_t)it * K * T, sigma, B, T, temperature, d_q,
+                            d_xp, d_cost, d_part, d_flag + it, 0, st);
+  std::vector<int32_t> flags(iters > 0 ? iters : 1, 0);
+  if (rc == VPM_OK) {
+    CK(cudaMemcpyAsync(u_star, d_u, T * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (iters > 0) CK(cudaMemcpyAsync(flags.data(), d_flag, iters * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  }
+  cudaFreeAsync(d_x0, st);
+  cudaFreeAsync(d_u, st);
+  cudaFreeAsync(d_noise, st);
+  cudaFreeAsync(d_q, st);
+  cudaFreeAsync(d_xp, st);
+  cudaFreeAsync(d_cost, st);
+  cudaFreeAsync(d_part, st);
+  cudaFreeAsync(d_flag, st);
+  CK(cudaStreamSynchronize(st));
+  CK(cudaStreamDestroy(st));
+  if (rc) return rc;
+  for (int it = 0; it < iters; ++it)
+    if (flags[it]) {
+      g_err = "all sampled rollouts failed (infinite cost)";
+      return VPM_ERR_ALLFAIL;
+    }
+  return VPM_OK;
+}
+
+int vpm_plan_timing(vpm_plan *p, int reset, double *avg_ms, int64_t *launches) {
+  if (!p) return fail_cfg("null plan");
+  CK(cudaSetDevice(p->device));
+  double tot = 0.0;
+  int64_t n = 0;
+  for (size_t i = 0; i + 1 < p->ev_used; i += 2) {
+    CK(cudaEventSynchronize(p->ev[i + 1]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]));
+    tot += ms;
+    ++n;
+  }
+  if (avg_ms) *avg_ms = n ? tot / n : 0.0;
+  if (launches) *launches = n;
+  if (reset) {
+    p->ev_used = 0;
+    p->timing = reset > 0;  // reset=1: start timing; reset=-1: stop timing
+  }
+  return VPM_OK;
+}
+
+double vpm_fp32_peak_probe(int iters) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1.0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = sms * 8, threads = 256;
+  float *d = nullptr;
+  if (cudaMalloc(&d, blocks * sizeof(float)) != cudaSuccess) return -1.0;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  vpm::fp32_probe_kernel<<<blocks, threads>>>(d, iters / 4, 0.9999f, 1e-4f);  // warm-up
+  cudaEventRecord(a);
+  vpm::fp32_probe_kernel<<<blocks, threads>>>(d, iters, 0.9999f, 1e-4f);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(d);
+  const double flops = 2.0 * 8.0 * (double)iters * blocks * threads;
+  return ms > 0.f ? flops / (ms * 1e-3) / 1e9 : -1.0;
+}
+
+int vpm_boundary_inverse(const int64_t *iparams, const double *fparams, double *out) {
+  Phys P;
+  int rc = unpack(iparams, fparams, &P);
+  if (rc) return rc;
+  std::vector<double> inv;
+  rc = build_inverses(P, inv);
+  if (rc) return rc;
+  std::memcpy(out, inv.data(), inv.size() * sizeof(double));
+  return VPM_OK;
+}
+
+int vpm_threads(void) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms * 8;
+}
+
+}  // extern "C"
+
+// ======================= reference-facing host-buffer layer ==========================
+namespace {
+
+// One cached plan per (thread, parameter set); host calls from several Python
+// threads (threaded NMPC, nmpc.py:219-222) get independent plans and streams.
+struct HostCtx {
+  std::vector<int64_t> ip;
+  std::vector<double> fp;
+  vpm_plan *plan = nullptr;
+  cudaStream_t st = nullptr;
+  void *scratch = nullptr;
+  size_t scratch_len = 0;
+};
+thread_local HostCtx g_host;
+
+int host_plan(const int64_t *ip, const double *fp, vpm_plan **out, cudaStream_t *st) {
+  HostCtx &h = g_host;
+  const bool same = h.plan && std::memcmp(h.ip.data(), ip, 2 * sizeof(int64_t)) == 0 &&
+                    std::memcmp(h.fp.data(), fp, FP_COUNT * sizeof(double)) == 0;
+  if (!same) {
+    if (h.plan) vpm_plan_destroy(h.plan);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    h.plan = vpm_plan_create(ip, fp, 0, 0, dev);
+    if (!h.plan) return VPM_ERR_CONFIG;
+    h.ip.assign(ip, ip + 2);
+    h.fp.assign(fp, fp + FP_COUNT);
+  }
+  if (!h.st) CK(cudaStreamCreateWithFlags(&h.st, cudaStreamNonBlocking));
+  *out = h.plan;
+  *st = h.st;
+  return VPM_OK;
+}
+
+void *host_scratch(size_t bytes) {
+  HostCtx &h = g_host;
+  if (h.scratch_len < bytes) {
+    cudaFree(h.scratch);
+    h.scratch = nullptr;
+    if (cudaMalloc(&h.scratch, bytes) != cudaSuccess) {
+      h.scratch_len = 0;
+      return nullptr;
+    }
+    h.scratch_len = bytes;
+  }
+  return h.scratch;
+}
+
+struct Carve {
+  char *base;
+  size_t off = 0;
+  template <class T>
+  T *take(size_t n) {
+    off = (off + 255) & ~(size_t)255;
+    T *p = reinterpret_cast<T *>(base + off);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+// Shared driver for step / rollout / batch_rollout with host buffers.
+int host_run(const double *x0, int x0_stride, const double *controls, int B, int T,
+             const vpm_fluid *fluid, const int64_t *ip, const double *fp, int integrate,
+             int check_env, int record, int64_t *status, double *finals, double *trajs,
+             int32_t *rc_out, double *fw_out, vpm_fluid_out *fo) {
+  Phys P;
+  int rc = unpack(ip, fp, &P);
+  if (rc) return rc;
+  if (B < 0 || T < 0) return fail_cfg("negative batch or horizon");
+  vpm_plan *p;
+  cudaStream_t st;
+  rc = host_plan(ip, fp, &p, &st);
+  if (rc) return rc;
+  rc = vpm_plan_set_fluid(p, fluid);
+  if (rc) return rc;
+  if (B == 0) return VPM_OK;
+  const int cap4 = P.cap + 4, nb = P.nb;
+  const size_t ntraj = record ? (size_t)B * (T + 1) * 7 : 0;
+  const size_t need = 256 * 16 + sizeof(double) * ((size_t)B * 7 + (size_t)B * T + (size_t)B * 7 + ntraj + 3 * (size_t)B +
+                                                   3 * cap4 + 4 * nb + 1) +
+                      sizeof(int64_t) * ((size_t)B + cap4) + sizeof(int32_t) * ((size_t)B + 4);
+  void *sc = host_scratch(need);
+  if (!sc) return fail_cfg("device scratch allocation failed");
+  Carve cv{(char *)sc};
+  double *d_x0 = cv.take<double>((size_t)(x0_stride ? B : 1) * 7);
+  double *d_ctrl = cv.take<double>((size_t)B * (T > 0 ? T : 1));
+  double *d_fin = cv.take<double>((size_t)B * 7);
+  double *d_traj = record ? cv.take<double>(ntraj) : nullptr;
+  double *d_fw = cv.take<double>((size_t)B * 3);
+  int64_t *d_st = cv.take<int64_t>(B);
+  int32_t *d_rc = cv.take<int32_t>(B);
+  Args a = base_args(p);
+  a.x0 = d_x0;
+  a.x0_stride = x0_stride;
+  a.controls = d_ctrl;
+  a.T = T;
+  a.rows = B;
+  a.integrate = integrate;
+  a.check_envelope = check_env;
+  a.record = record;
+  a.status = d_st;
+  a.finals = d_fin;
+  a.trajs = d_traj;
+  a.rc_out = d_rc;
+  a.fw_out = d_fw;
+  if (fo) {
+    a.need_fluid = 1;
+    a.o_wpos = cv.take<double>(2 * (size_t)cap4);
+    a.o_wgam = cv.take<double>(cap4);
+    a.o_wage = cv.take<int64_t>(cap4);
+    a.o_scal = cv.take<int32_t>(4);
+    a.o_ppos = cv.take<double>(2 * (size_t)nb);
+    a.o_pgam = cv.take<double>(nb);
+    a.o_plev = cv.take<double>(1);
+    a.o_ema = cv.take<double>(nb);
+  }
+  CK(cudaMemcpyAsync(d_x0, x0, sizeof(double) * (x0_stride ? B : 1) * 7, cudaMemcpyHostToDevice, st));
+  if (T > 0) CK(cudaMemcpyAsync(d_ctrl, controls, sizeof(double) * (size_t)B * T, cudaMemcpyHostToDevice, st));
+  if (record) CK(cudaMemsetAsync(d_traj, 0, sizeof(double) * ntraj, st));
+  rc = plan_launch(p, a, B, st);
+  if (rc) return rc;
+  if (status) CK(cudaMemcpyAsync(status, d_st, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, st));
+  if (rc_out) CK(cudaMemcpyAsync(rc_out, d_rc, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+  if (finals) CK(cudaMemcpyAsync(finals, d_fin, sizeof(double) * B * 7, cudaMemcpyDeviceToHost, st));
+  if (trajs && record) CK(cudaMemcpyAsync(trajs, d_traj, sizeof(double) * ntraj, cudaMemcpyDeviceToHost, st));
+  if (fw_out) CK(cudaMemcpyAsync(fw_out, d_fw, sizeof(double) * 3, cudaMemcpyDeviceToHost, st));
+  if (fo) {
+    CK(cudaMemcpyAsync(fo->wake_pos, a.o_wpos, sizeof(double) * 2 * cap4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fo->wake_gamma, a.o_wgam, sizeof(double) * cap4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fo->wake_age, a.o_wage, sizeof(int64_t) * cap4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fo->scalars, a.o_scal, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fo->prev_pos, a.o_ppos, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fo->prev_gamma, a.o_pgam, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fo->prev_lev, a.o_plev, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fo->ema, a.o_ema, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return VPM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vpm_step(double *x, double u, const vpm_fluid *fluid, const int64_t *iparams,
+             const double *fparams, int integrate, double *fw, double *mw, vpm_fluid_out *out) {
+  int64_t status = 0;
+  int32_t rc = 0;
+  double fwm[3] = {0.0, 0.0, 0.0};
+  double xn[7];
+  int e = host_run(x, 0, &u, 1, 1, fluid, iparams, fparams, integrate, 0, 0, &status, xn, nullptr,
+                   &rc, fwm, out);
+  if (e) return e;
+  std::memcpy(x, xn, sizeof(xn));
+  if (fw) { fw[0] = fwm[0]; fw[1] = fwm[1]; }
+  if (mw) *mw = fwm[2];
+  return status == 0 ? 0 : (rc ? rc : 1);
+}
+
+int64_t vpm_rollout(double *x, const double *controls, int T, const vpm_fluid *fluid,
+                    const int64_t *iparams, const double *fparams, double *traj,
+                    vpm_fluid_out *out) {
+  int64_t status = 0;
+  double xn[7];
+  int e = host_run(x, 0, controls, 1, T, fluid, iparams, fparams, 1, 1, traj != nullptr, &status, xn,
+                   traj, nullptr, nullptr, out);
+  if (e) return e;
+  std::memcpy(x, xn, sizeof(xn));
+  return status;
+}
+
+int vpm_batch_rollout(const double *x0, const double *controls, int B, int T,
+                      const vpm_fluid *fluid, const int64_t *iparams, const double *fparams,
+                      int record, int workers, int64_t *status, double *finals, double *trajs) {
+  (void)workers;
+  return host_run(x0, 0, controls, B, T, fluid, iparams, fparams, 1, 1, record, status, finals,
+                  trajs, nullptr, nullptr, nullptr);
+}
+
+// Batched rollouts with one start state per row (policy synthesis cloud,
+// policy.py:66-91) plus the discrete-decision diagnostics used by the parity
+// harness.  x0 is (B, 7).
+int vpm_batch_rollout_x0(const double *x0, const double *controls, int B, int T,
+                         const vpm_fluid *fluid, const int64_t *iparams, const double *fparams,
+                         int record, int64_t *status, double *finals, double *trajs) {
+  return host_run(x0, 7, controls, B, T, fluid, iparams, fparams, 1, 1, record, status, finals,
+                  trajs, nullptr, nullptr, nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,927 @@
+// vpm_rollout.cuh -- sm_100a kernels of the VPM-MPPI hot path.
+//
+// One CTA owns one rollout for all H steps.  The wake (<= cap+8 particles) lives
+// in shared memory as float4 {x, z, Gamma/(2 pi), age}; the rigid-body state, the
+// bound-vortex row, the unsteady-load filter and every discrete decision live in
+// a small FP64 control block in shared memory.  The O(N^2) regularised
+// Biot-Savart sweeps run on the FP32 pipe (FFMA + MUFU.RSQ), everything O(1) /
+// O(nb) runs in FP64 on warp 0.
+//
+// Reference semantics (paths relative to /root/reference/pkg/src/perchsim/):
+//   step_core         _accel/_core.pyx:175-462  (== vpm.py:635-669 + glider.py:104-122)
+//   run_rollout       _accel/_core.pyx:465-491
+//   batch_rollout     _accel/_core.pyx:664-741
+//   terminal cost     mppi.py:28-34
+//   MPPI update       mppi.py:46-59
+//
+// Per-step phase schedule inside the CTA (barriers B1..B4):
+//
+//   S1  all threads: velocity at every live wake particle from every wake
+//       particle + the previous bound row (convection of step t, _core.pyx:192-221)
+//       and, source-split, the wake velocity at the panels of step t-1 (the loads
+//       of step t-1, _core.pyx:385-389 -- same sources: the post-merge wake).
+//   B1
+//   D   warp 0: unsteady-Bernoulli loads of step t-1 (_core.pyx:375-418),
+//       elevator + Euler integration (_core.pyx:423-461), envelope check
+//       (_core.pyx:483-484), then the chord frame / collocation geometry and the
+//       stall + reversed-flow gates of step t (_core.pyx:228-256).
+//   A   all threads (overlapping D): Euler advection, dissipation, ageing of
+//       their own particles (_core.pyx:222-226), written straight into their
+//       compacted slot (this retires the ordered removals of step t-1); Kelvin
+//       partial sums; per-warp merge candidates.
+//   B2
+//   S2  all threads: wake velocity at the nb collocation rows (_core.pyx:273-296).
+//   B3
+//   E   warp 0: right-hand side, bound-circulation solve with the precomputed
+//       inverse of the pose-invariant system, shed LEV/TEV
+//       (_core.pyx:322-334), merge of the oldest particles (_core.pyx:336-357)
+//       as a top-(m+1) selection, ring termination (_core.pyx:359-373).  Removed
+//       particles become zero-circulation holes until the next A compacts them.
+//   B4
+//
+// The loads of step t are computed lazily at the top of iteration t+1 because
+// they need exactly the sources of the next convection sweep.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+namespace vpm {
+
+constexpr int NB_MAX = 64;  // reference MAXNB (_core.pyx:23)
+constexpr int NW_MAX = 16;  // up to 512 threads per rollout
+constexpr int MC = 8;       // merge candidates kept per warp
+constexpr int XMAX = 8;     // overflow wake targets handled source-split
+constexpr int CH = 4;       // source-split targets per chunk
+constexpr int HOLES_MAX = 16;
+constexpr int WAKE_PAD = 8;  // wake slots beyond cap (reference buffers hold cap+4)
+constexpr double TWO_PI = 6.283185307179586476925286766559;
+constexpr double INV_TWO_PI = 0.15915494309189533576888376337251;
+constexpr double PI = 3.14159265358979323846264338327950288;
+
+struct Phys {
+  int nb, cap;
+  double r_core, k_diss, shed_off, crit_aoa, rho, dt, m, inertia, g, l, l_w, l_e, l_chord, s_e,
+      phi_lim, u_lim, lev_gain, eta;
+  float rc4f;
+};
+
+struct Args {
+  Phys P;
+  const double *ainv;  // 3 variants x (nb+2)^2, row-major; variant 0 (attached) stride nb
+  // fluid snapshot, FP64 reference layout
+  const double *wpos, *wgam;
+  const int64_t *wage;
+  int n_wake, ring_a, ring_b;
+  const double *ppos, *pgam;
+  int n_prev;
+  double prev_lev;
+  const double *ema;
+  // start state
+  const double *x0;
+  int x0_stride;
+  // controls: explicit rows, or MPPI sampling from u* and noise
+  const double *controls;
+  const double *ustar, *noise;
+  double sigma;
+  int T, row_begin, rows;
+  int integrate, check_envelope, need_fluid, record;
+  // outputs (any may be null)
+  int64_t *status;
+  double *finals, *trajs, *cost;
+  const double *q, *xp;
+  uint64_t *shed_mask;
+  int32_t *n_final;
+  int64_t *inter;
+  int32_t *rc_out;
+  double *fw_out;  // (rows, 3): fw_x, fw_z, m_w of the last completed step
+  double *o_wpos, *o_wgam;
+  int64_t *o_wage;
+  int32_t *o_scal;
+  double *o_ppos, *o_pgam, *o_plev, *o_ema;
+};
+
+struct Ctl {
+  double x[7];
+  double u;
+  double fx, fz, nx, nz, s;
+  double lx, lz, tx, tz;
+  double lev_cur, lev_prev;
+  double fwx, fwz, mw;
+  int shed, rev;
+  int hp;       // has_prev for the pending step's loads (n_prev > 0 at its start)
+  int n_prev;   // rows in the previous bound row (0 or nb)
+  int pending;  // loads + integration of the last solved step not yet applied
+  int n_raw, n_live, ring_a, ring_b, n_holes;
+  int holes[HOLES_MAX];
+  int np_split, nx_split;  // split targets of the next S1: panels, overflow particles
+  int mcnt;                // merge candidates each warp keeps this step
+  int fail, status, rc;
+  long long inter;
+  unsigned long long shed_mask;
+};
+
+// ---- shared-memory layout (host computes the same size) ----------------------
+struct Layout {
+  int capbuf, nb, S, RS, nw;
+  int off_psrc, off_st, off_ctl, off_d, off_cand, total;
+};
+
+__host__ __device__ inline int align16(int v) { return (v + 15) & ~15; }
+
+__host__ __device__ inline Layout make_layout(int cap, int nb, int nt) {
+  Layout L;
+  L.capbuf = cap + WAKE_PAD;
+  L.nb = nb;
+  L.S = nb + 2;
+  L.RS = 2 * (nb + XMAX);
+  L.nw = nt / 32;
+  int off = L.capbuf * 16;
+  L.off_psrc = off;
+  off += nb * 16;
+  L.off_st = off;
+  off += (nb + XMAX) * 8;
+  off = align16(off);
+  L.off_ctl = off;
+  off += align16((int)sizeof(Ctl));
+  L.off_d = off;
+  // cx cz bx bz gam pgp pxp pzp ema bvec (10 S) + pf (3 S) + kel (nw) + red (nw RS)
+  off += (13 * L.S + L.nw + L.nw * L.RS) * 8;
+  off = align16(off);
+  L.off_cand = off;
+  off += L.nw * MC * 4;
+  L.total = align16(off);
+  return L;
+}
+
+// ---- device helpers ------------------------------------------------------------
+__device__ __forceinline__ float rsqrt_mufu(float v) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+// u += g' [dz, -dx] / sqrt(r^4 + rc^4), g' = Gamma / 2pi   (_core.pyx:89-97)
+__device__ __forceinline__ void bs_accum(float sx, float sz, float sg, float tx, float tz,
+                                         float rc4, float &ux, float &uz) {
+  const float dx = tx - sx;
+  const float dz = tz - sz;
+  const float r2 = fmaf(dx, dx, dz * dz);
+  const float c = sg * rsqrt_mufu(fmaf(r2, r2, rc4));
+  ux = fmaf(c, dz, ux);
+  uz = fmaf(-c, dx, uz);
+}
+
+// Register-tiled sweep: K targets per thread against n sources in shared memory.
+template <int K>
+__device__ __forceinline__ void sweep_tile(const float4 *__restrict__ src, int n,
+                                           const float *tx, const float *tz, float *ux,
+                                           float *uz, float rc4) {
+#pragma unroll 4
+  for (int j = 0; j < n; ++j) {
+    const float4 s = src[j];
+#pragma unroll
+    for (int k = 0; k < K; ++k) bs_accum(s.x, s.y, s.z, tx[k], tz[k], rc4, ux[k], uz[k]);
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void sweep_dispatch(int kw, const float4 *src, int n, const float *tx,
+                                               const float *tz, float *ux, float *uz, float rc4) {
+  // kw = number of target slots live in this warp (warp-uniform)
+  if constexpr (R >= 8) {
+    if (kw == 8) { sweep_tile<8>(src, n, tx, tz, ux, uz, rc4); return; }
+    if (kw == 7) { sweep_tile<7>(src, n, tx, tz, ux, uz, rc4); return; }
+    if (kw == 6) { sweep_tile<6>(src, n, tx, tz, ux, uz, rc4); return; }
+    if (kw == 5) { sweep_tile<5>(src, n, tx, tz, ux, uz, rc4); return; }
+  }
+  if constexpr (R >= 4) {
+    if (kw == 4) { sweep_tile<4>(src, n, tx, tz, ux, uz, rc4); return; }
+    if (kw == 3) { sweep_tile<3>(src, n, tx, tz, ux, uz, rc4); return; }
+  }
+  if constexpr (R >= 2) {
+    if (kw == 2) { sweep_tile<2>(src, n, tx, tz, ux, uz, rc4); return; }
+  }
+  if (kw >= 1) sweep_tile<1>(src, n, tx, tz, ux, uz, rc4);
+}
+
+// Deterministic butterfly-transpose reduction of 8 floats across a warp:
+// afterwards every lane holds the full sum of value index (lane >> 2).
+__device__ __forceinline__ float warp_reduce8(float v[8], int lane) {
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = h16 ? v[i] : v[i + 4];
+    const float keep = h16 ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = h8 ? v[i] : v[i + 2];
+    const float keep = h8 ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const float send = h4 ? v[0] : v[1];
+    const float keep = h4 ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return v[0];
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// raw slot of the c-th live particle, skipping the sorted hole list
+__device__ __forceinline__ int raw_index(int c, const int *holes, int nh) {
+  int r = c;
+  for (int h = 0; h < nh; ++h)
+    if (holes[h] <= r) ++r;
+  return r;
+}
+
+// Source-split sweep: targets tgt[0..nt) (float2), every thread takes sources
+// j = tid, tid+NT, ... of src[0..n); per-warp sums land in red[warp*RS + 2k(+1)].
+template <int NT>
+__device__ __forceinline__ void split_sweep(const float4 *__restrict__ src, int n,
+                                            const float2 *tgt, int nt, float rc4, double *red,
+                                            int RS, int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int c0 = 0; c0 < nt; c0 += CH) {
+    float tx[CH], tz[CH];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int i = c0 + k < nt ? c0 + k : nt - 1;
+      tx[k] = tgt[i].x;
+      tz[k] = tgt[i].y;
+    }
+    float acc[2 * CH];
+#pragma unroll
+    for (int k = 0; k < 2 * CH; ++k) acc[k] = 0.f;
+    for (int j = tid; j < n; j += NT) {
+      const float4 s = src[j];
+#pragma unroll
+      for (int k = 0; k < CH; ++k) bs_accum(s.x, s.y, s.z, tx[k], tz[k], rc4, acc[2 * k], acc[2 * k + 1]);
+    }
+    const float r = warp_reduce8(acc, lane);
+    const int vi = lane >> 2;  // value index: target c0 + vi/2, component vi&1
+    if ((lane & 3) == 0 && c0 + (vi >> 1) < nt) red[warp * RS + 2 * c0 + vi] = (double)r;
+  }
+}
+
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {
+  return v > hi ? hi : (v < lo ? lo : v);
+}
+
+// control of global candidate row g at step t (mppi.py:37-43, :79; _core.pyx:183-187)
+__device__ __forceinline__ double control_at(const Args &a, int row, int t) {
+  double u;
+  if (a.controls) {
+    u = a.controls[(size_t)row * a.T + t];
+  } else {
+    const int g = a.row_begin + row;
+    u = a.ustar[t];
+    if (g > 0) u = clampd(u + a.noise[(size_t)(g - 1) * a.T + t] * a.sigma, -a.P.u_lim, a.P.u_lim);
+  }
+  return u;
+}
+
+// ---- the rollout kernel -------------------------------------------------------------
+template <int NT, int R>
+__global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Phys &P = a.P;
+  const int nb = P.nb;
+  const Layout L = make_layout(P.cap, nb, NT);
+  float4 *wk = reinterpret_cast<float4 *>(smem);
+  float4 *psrc = reinterpret_cast<float4 *>(smem + L.off_psrc);
+  float2 *st = reinterpret_cast<float2 *>(smem + L.off_st);
+  Ctl *ctl = reinterpret_cast<Ctl *>(smem + L.off_ctl);
+  double *dsh = reinterpret_cast<double *>(smem + L.off_d);
+  const int S = L.S, RS = L.RS;
+  double *cx = dsh, *cz = dsh + S, *bx = dsh + 2 * S, *bz = dsh + 3 * S, *gam = dsh + 4 * S;
+  double *pgp = dsh + 5 * S, *pxp = dsh + 6 * S, *pzp = dsh + 7 * S, *ema = dsh + 8 * S;
+  double *bvec = dsh + 9 * S, *pf = dsh + 10 * S, *kel = dsh + 13 * S, *red = kel + NW;
+  unsigned *cand = reinterpret_cast<unsigned *>(smem + L.off_cand);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row = blockIdx.x;
+  const int T = a.T;
+  const float rc4 = P.rc4f;
+  const double dt = P.dt;
+  constexpr int TILE = NT * R;
+
+  // ---- prologue: fork the snapshot into shared memory (_core.pyx:494-526)
+  for (int i = tid; i < a.n_wake; i += NT)
+    wk[i] = make_float4((float)a.wpos[2 * i], (float)a.wpos[2 * i + 1],
+                        (float)(a.wgam[i] * INV_TWO_PI), __int_as_float((int)a.wage[i]));
+  for (int j = tid; j < a.n_prev; j += NT)
+    psrc[j] = make_float4((float)a.ppos[2 * j], (float)a.ppos[2 * j + 1],
+                          (float)(a.pgam[j] * INV_TWO_PI), 0.f);
+  if (warp == 0) {
+    for (int j = lane; j < nb; j += 32) {
+      const bool have = j < a.n_prev;
+      pgp[j] = have ? a.pgam[j] : 0.0;
+      pxp[j] = have ? a.ppos[2 * j] : 0.0;
+      pzp[j] = have ? a.ppos[2 * j + 1] : 0.0;
+      ema[j] = a.ema[j];
+    }
+    const double *x0 = a.x0 + (size_t)row * a.x0_stride;
+    if (lane < 7) {
+      ctl->x[lane] = x0[lane];
+      if (a.record && a.trajs) a.trajs[(size_t)row * (T + 1) * 7 + lane] = x0[lane];
+    }
+    const int xs = a.n_wake > TILE ? min(XMAX, a.n_wake - TILE) : 0;
+    if (lane < xs) st[lane] = make_float2((float)a.wpos[2 * (TILE + lane)], (float)a.wpos[2 * (TILE + lane) + 1]);
+    if (lane == 0) {
+      ctl->n_raw = a.n_wake;
+      ctl->n_live = a.n_wake;
+      ctl->n_holes = 0;
+      ctl->ring_a = a.ring_a;
+      ctl->ring_b = a.ring_b;
+      ctl->n_prev = a.n_prev;
+      ctl->lev_prev = a.prev_lev;
+      ctl->lev_cur = 0.0;
+      ctl->pending = 0;
+      ctl->np_split = 0;
+      ctl->nx_split = xs;
+      ctl->mcnt = min(MC, max(0, a.n_wake + 3 - P.cap));
+      ctl->fail = 0;
+      ctl->status = 0;
+      ctl->rc = 0;
+      ctl->inter = 0;
+      ctl->shed_mask = 0ull;
+      ctl->fwx = ctl->fwz = ctl->mw = 0.0;
+      ctl->hp = 0;
+      ctl->shed = ctl->rev = 0;
+    }
+  }
+  __syncthreads();
+
+  for (int t = 0;; ++t) {
+    const bool conv = t < T;
+    const bool pend = ctl->pending;
+    const int n_raw = ctl->n_raw, n_live = ctl->n_live, nh = ctl->n_holes;
+    const int np_s = pend ? ctl->np_split : 0;
+    const int nx_s = conv ? ctl->nx_split : 0;
+    const int n_prev = ctl->n_prev;
+
+    // ---------------- S1: convection sweep (+ loads sweep of step t-1)
+    float tx[R], tz[R], tg[R], ux[R], uz[R];
+    int tage[R];
+    int kw = 0;
+    if (conv) {
+      const int nwt = min(n_live, TILE);
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int c = tid + NT * k;
+        ux[k] = 0.f;
+        uz[k] = 0.f;
+        if (c < nwt) {
+          const float4 v = wk[raw_index(c, ctl->holes, nh)];
+          tx[k] = v.x; tz[k] = v.y; tg[k] = v.z; tage[k] = __float_as_int(v.w);
+        } else {
+          tx[k] = 0.f; tz[k] = 0.f; tg[k] = 0.f; tage[k] = 0;
+        }
+      }
+      const int wbase = warp * 32;
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (wbase + NT * k < nwt) kw = k + 1;
+      sweep_dispatch<R>(kw, wk, n_raw, tx, tz, ux, uz, rc4);
+      sweep_dispatch<R>(kw, psrc, n_prev, tx, tz, ux, uz, rc4);
+    }
+    if (np_s + nx_s > 0) split_sweep<NT>(wk, n_raw, st, np_s + nx_s, rc4, red, RS, tid);
+    __syncthreads();  // B1
+
+    // ---------------- D: loads + integration of step t-1, geometry of step t
+    if (warp == 0) {
+      if (pend) {
+        const double fx = ctl->fx, fz = ctl->fz, nx = ctl->nx, nz = ctl->nz, s = ctl->s;
+        const double rx = ctl->x[0], rz = ctl->x[1], vx = ctl->x[4], vz = ctl->x[5], om = ctl->x[6];
+        const int hp = ctl->hp;
+        const double xwx = rx - P.l_w * fx, xwz = rz - P.l_w * fz;
+        const double dlev = hp ? (ctl->lev_cur - ctl->lev_prev) / dt : 0.0;
+        for (int p = lane; p < nb; p += 32) {
+          double uxp = 0.0, uzp = 0.0;
+          for (int w = 0; w < NW; ++w) { uxp += red[w * RS + 2 * p]; uzp += red[w * RS + 2 * p + 1]; }
+          double cum = 0.0, cum_prev = 0.0;
+          for (int i = 0; i <= p; ++i) { cum += gam[i]; cum_prev += pgp[i]; }
+          const double rate = hp ? (cum - cum_prev) / dt + dlev : 0.0;
+          const double e = P.eta * rate + (1.0 - P.eta) * (hp ? ema[p] : 0.0);
+          const double svx = vx + om * (-(bz[p] - rz)), svz = vz + om * (bx[p] - rx);
+          const double beta = (uxp - svx) * fx + (uzp - svz) * fz;
+          const double dp = P.rho * (beta * gam[p] / s + e);
+          const double pfx = dp * s * nx, pfz = dp * s * nz;
+          pf[3 * p] = pfx;
+          pf[3 * p + 1] = pfz;
+          pf[3 * p + 2] = (bx[p] - xwx) * pfz - (bz[p] - xwz) * pfx;
+          ema[p] = e;
+        }
+        __syncwarp();
+        for (int p = lane; p < nb; p += 32) { pgp[p] = gam[p]; pxp[p] = bx[p]; pzp[p] = bz[p]; }
+        if (lane == 0) {
+          double Fx = 0.0, Fz = 0.0, M = 0.0;
+          for (int p = 0; p < nb; ++p) { Fx += pf[3 * p]; Fz += pf[3 * p + 1]; M += pf[3 * p + 2]; }
+          ctl->fwx = Fx; ctl->fwz = Fz; ctl->mw = M;
+          ctl->lev_prev = ctl->lev_cur;
+          ctl->pending = 0;
+          if (a.integrate) {
+            // elevator + accelerations + forward Euler (_core.pyx:423-461)
+            const double th = ctl->x[2], phi = ctl->x[3], u = ctl->u;
+            double se, ce;
+            sincos(th + phi, &se, &ce);
+            const double fex = ce, fez = se, nex = -se, nez = ce;
+            const double xex = rx - P.l * fx - P.l_e * fex, xez = rz - P.l * fz - P.l_e * fez;
+            const double vex = vx - P.l * om * nx - P.l_e * (om + u) * nex;
+            const double vez = vz - P.l * om * nz - P.l_e * (om + u) * nez;
+            const double sp2 = vex * vex + vez * vez;
+            double Ex = 0.0, Ez = 0.0;
+            if (sp2 >= 1e-18) {
+              const double ae = th + phi - atan2(vez, vex);
+              const double cn = 0.5 * P.rho * sp2 * P.s_e * 2.0 * sin(ae);
+              Ex = cn * nex; Ez = cn * nez;
+            }
+            const double ax = (Fx + Ex) / P.m;
+            const double az = (Fz + Ez) / P.m - P.g;
+            const double tq = M + ((xwx - rx) * Fz - (xwz - rz) * Fx) + ((xex - rx) * Ez - (xez - rz) * Ex);
+            const double wd = tq / P.inertia;
+            double xn[7];
+            xn[0] = rx + dt * vx;
+            xn[1] = rz + dt * vz;
+            xn[2] = th + dt * om;
+            xn[3] = clampd(phi + dt * u, -P.phi_lim, P.phi_lim);
+            xn[4] = vx + dt * ax;
+            xn[5] = vz + dt * az;
+            xn[6] = om + dt * wd;
+            bool fin = true;
+            for (int i = 0; i < 7; ++i) { ctl->x[i] = xn[i]; fin = fin && isfinite(xn[i]); }
+            if (!fin) {
+              ctl->fail = 1; ctl->status = t; ctl->rc = 2;
+            } else if (a.check_envelope && (fabs(xn[6]) > 300.0 || fabs(xn[4]) > 80.0 || fabs(xn[5]) > 80.0)) {
+              ctl->fail = 1; ctl->status = t; ctl->rc = 0;
+            }
+          }
+        }
+        __syncwarp();
+        if (a.record && a.trajs && lane < 7 && !ctl->fail)
+          a.trajs[((size_t)row * (T + 1) + t) * 7 + lane] = ctl->x[lane];
+      }
+      if (conv && !ctl->fail) {
+        // chord frame, collocation points, gates of step t (_core.pyx:228-256)
+        const double rx = ctl->x[0], rz = ctl->x[1], th = ctl->x[2];
+        const double vx = ctl->x[4], vz = ctl->x[5], om = ctl->x[6];
+        double sn, cs;
+        sincos(th, &sn, &cs);
+        const double fx = cs, fz = sn, nx = -sn, nz = cs;
+        const double s = P.l_chord / nb;
+        for (int i = lane; i <= nb; i += 32) { cx[i] = rx - fx * s * i; cz[i] = rz - fz * s * i; }
+        for (int j = lane; j < nb; j += 32) {
+          const double c0x = rx - fx * s * j, c0z = rz - fz * s * j;
+          bx[j] = c0x - 0.5 * s * fx;
+          bz[j] = c0z - 0.5 * s * fz;
+        }
+        double aoa = 0.0;
+        const double vwx = vx - P.l_w * om * nx, vwz = vz - P.l_w * om * nz;
+        if (vwx * vwx + vwz * vwz >= 1e-18) {
+          const double raw = th - atan2(vwz, vwx);
+          double sr, cr;
+          sincos(raw, &sr, &cr);
+          aoa = atan2(sr, cr);
+        }
+        if (lane == 0) {
+          ctl->fx = fx; ctl->fz = fz; ctl->nx = nx; ctl->nz = nz; ctl->s = s;
+          ctl->lx = rx + P.shed_off * fx;
+          ctl->lz = rz + P.shed_off * fz;
+          ctl->tx = (rx - fx * s * nb) - P.shed_off * fx;
+          ctl->tz = (rz - fz * s * nb) - P.shed_off * fz;
+          ctl->shed = fabs(aoa) > P.crit_aoa;
+          ctl->rev = fabs(aoa) > 0.5 * PI;
+          const double u = control_at(a, row, t);
+          ctl->u = clampd(u, -P.u_lim, P.u_lim);
+        }
+      }
+    }
+
+    // ---------------- A: advect / dissipate / age into compacted slots
+    if (conv) {
+      if (a.need_fluid) {
+        __syncthreads();
+        if (ctl->fail) break;
+      }
+      const int ra = ctl->ring_a, rb = ctl->ring_b;
+      const int nwt = min(n_live, TILE);
+      double ksum = 0.0;
+      unsigned keys[R + 1];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int c = tid + NT * k;
+        keys[k] = 0u;
+        if (c < nwt) {
+          const float nxp = (float)((double)tx[k] + dt * (double)ux[k]);
+          const float nzp = (float)((double)tz[k] + dt * (double)uz[k]);
+          const float ng = (float)((double)tg[k] * P.k_diss);
+          const int na = tage[k] + 1;
+          wk[c] = make_float4(nxp, nzp, ng, __int_as_float(na));
+          ksum += (double)ng;
+          if (c != ra && c != rb) keys[k] = ((unsigned)(na + 1) << 12) | (unsigned)(4095 - c);
+        }
+      }
+      keys[R] = 0u;
+      if (warp == 0 && nx_s > 0) {
+        // overflow particles beyond the register tile (only when n_live > NT*R)
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        int c = TILE + lane;
+        float vx = 0.f, vz = 0.f;
+        if (lane < nx_s) {
+          v = wk[raw_index(c, ctl->holes, nh)];
+          double sx = 0.0, sz = 0.0;
+          for (int w = 0; w < NW; ++w) { sx += red[w * RS + 2 * (np_s + lane)]; sz += red[w * RS + 2 * (np_s + lane) + 1]; }
+          vx = (float)sx; vz = (float)sz;
+          for (int j = 0; j < n_prev; ++j) { const float4 p = psrc[j]; bs_accum(p.x, p.y, p.z, v.x, v.y, rc4, vx, vz); }
+        }
+        __syncwarp();
+        if (lane < nx_s) {
+          const float ng = (float)((double)v.z * P.k_diss);
+          const int na = __float_as_int(v.w) + 1;
+          wk[c] = make_float4((float)((double)v.x + dt * (double)vx), (float)((double)v.y + dt * (double)vz), ng, __int_as_float(na));
+          ksum += (double)ng;
+          if (c != ra && c != rb) keys[R] = ((unsigned)(na + 1) << 12) | (unsigned)(4095 - c);
+        }
+      }
+      ksum = warp_sum_d(ksum);
+      if (lane == 0) kel[warp] = ksum;
+      const int mc = ctl->mcnt;
+      for (int r = 0; r < mc; ++r) {
+        unsigned best = 0u;
+        int bi = -1;
+#pragma unroll
+        for (int k = 0; k <= R; ++k)
+          if (keys[k] > best) { best = keys[k]; bi = k; }
+        const unsigned w = __reduce_max_sync(0xffffffffu, best);
+        if (lane == 0) cand[warp * MC + r] = w;
+        if (w != 0u && best == w) {
+#pragma unroll
+          for (int k = 0; k <= R; ++k)
+            if (k == bi) keys[k] = 0u;
+        }
+      }
+    }
+    __syncthreads();  // B2
+    if (!conv || ctl->fail) break;
+
+    // ---------------- S2: wake velocity at the collocation rows of step t
+    {
+      const int shed_rev = ctl->shed && ctl->rev;
+      // rows: skip the upstream edge point (_core.pyx:274-275)
+      float2 *rows = st;  // reuse the split-target buffer (S1 consumers are done)
+      for (int i = tid; i < nb; i += NT) {
+        const int ri = shed_rev ? i : i + 1;
+        rows[i] = make_float2((float)cx[ri], (float)cz[ri]);
+      }
+      __syncthreads();
+      split_sweep<NT>(wk, ctl->n_live, rows, nb, rc4, red, RS, tid);
+    }
+    __syncthreads();  // B3
+
+    // ---------------- E: solve, shed, merge, ring termination (warp 0)
+    if (warp == 0) {
+      const int shed = ctl->shed, rev = ctl->rev;
+      const int ns = shed ? nb + 2 : nb, r0 = shed ? 1 : 0;
+      const int nl = ctl->n_live;
+      const double rx = ctl->x[0], rz = ctl->x[1], vx = ctl->x[4], vz = ctl->x[5], om = ctl->x[6];
+      const double nx = ctl->nx, nz = ctl->nz;
+      for (int i = lane; i < nb; i += 32) {
+        double uxw = 0.0, uzw = 0.0;
+        for (int w = 0; w < NW; ++w) { uxw += red[w * RS + 2 * i]; uzw += red[w * RS + 2 * i + 1]; }
+        const int ri = (shed && rev) ? i : i + 1;
+        const double px = cx[ri], pz = cz[ri];
+        const double svx = vx + om * (-(pz - rz)), svz = vz + om * (px - rx);
+        bvec[r0 + i] = (svx - uxw) * nx + (svz - uzw) * nz;
+      }
+      if (shed && lane == 0) {
+        const int epan = rev ? nb - 1 : 0;
+        bvec[0] = P.lev_gain * (ctl->n_prev > 0 ? pgp[epan] : 0.0);
+        double tot = 0.0;
+        for (int w = 0; w < NW; ++w) tot += kel[w];
+        bvec[nb + 1] = -(tot * TWO_PI);
+      }
+      __syncwarp();
+      const int var = shed ? (rev ? 2 : 1) : 0;
+      const double *Ai = a.ainv + (size_t)var * S * S;
+      bool ok = true;
+      for (int i = lane; i < ns; i += 32) {
+        double acc = 0.0;
+        for (int j = 0; j < ns; ++j) acc += Ai[i * ns + j] * bvec[j];
+        gam[i] = acc;
+        ok = ok && isfinite(acc);
+      }
+      ok = __all_sync(0xffffffffu, ok);
+      __syncwarp();
+      if (!ok) {
+        if (lane == 0) {
+          ctl->fail = 1; ctl->status = t + 1; ctl->rc = 2;
+          ctl->n_raw = nl; ctl->n_holes = 0;
+        }
+      } else {
+        const double levg = shed ? gam[nb] : 0.0;
+        int n_now = nl;
+        if (shed) {
+          if (lane == 0) wk[nl] = make_float4((float)ctl->lx, (float)ctl->lz, (float)(gam[nb] * INV_TWO_PI), __int_as_float(0));
+          if (lane == 1) wk[nl + 1] = make_float4((float)ctl->tx, (float)ctl->tz, (float)(gam[nb + 1] * INV_TWO_PI), __int_as_float(0));
+          n_now = nl + 2;
+        }
+        __syncwarp();
+        // ---- merge the oldest down to the cap: top-(m+1) by (age desc, index asc)
+        int nholes = 0;
+        int hl[HOLES_MAX];
+        const int m = n_now - P.cap;
+        int ra = ctl->ring_a, rb = ctl->ring_b;
+        if (m > 0) {
+          // gather the per-warp candidate lists: lane l holds entries l + 32 s
+          const int mcn = ctl->mcnt;
+          unsigned kk[5];
+#pragma unroll
+          for (int s4 = 0; s4 < 4; ++s4) {
+            const int idx = lane + 32 * s4;
+            kk[s4] = (mcn > 0 && idx < NW * mcn) ? cand[(idx / mcn) * MC + idx % mcn] : 0u;
+          }
+          // the particles shed this step (age 0, indices nl, nl+1) are candidates too
+          kk[4] = 0u;
+          if (shed && lane < 2) {
+            const int id = nl + lane;
+            if (id != ra && id != rb) kk[4] = (1u << 12) | (unsigned)(4095 - id);
+          }
+          unsigned sel[MC];
+          int nsel = 0;
+          for (int r = 0; r <= m && r < MC; ++r) {
+            unsigned mine = 0u;
+#pragma unroll
+            for (int s5 = 0; s5 < 5; ++s5) mine = max(mine, kk[s5]);
+            const unsigned w = __reduce_max_sync(0xffffffffu, mine);
+            if (w == 0u) break;
+            sel[nsel++] = w;
+#pragma unroll
+            for (int s5 = 0; s5 < 5; ++s5)
+              if (kk[s5] == w) kk[s5] = 0u;
+          }
+          if (nsel >= 2) {
+            const int merges = min(m, nsel - 1);
+            int idx0 = 4095 - (int)(sel[0] & 4095u);
+            float4 blob = wk[idx0];
+            int lo = idx0;
+            int ids[MC];
+            ids[0] = idx0;
+            for (int r = 1; r <= merges; ++r) {
+              const int id = 4095 - (int)(sel[r] & 4095u);
+              ids[r] = id;
+              const float4 p = wk[id];
+              blob.x = 0.5f * (blob.x + p.x);
+              blob.y = 0.5f * (blob.y + p.y);
+              blob.z = blob.z + p.z;
+              lo = min(lo, id);
+            }
+            __syncwarp();
+            if (lane == 0) wk[lo] = blob;
+            for (int r = 0; r <= merges; ++r)
+              if (ids[r] != lo) hl[nholes++] = ids[r];
+          }
+        }
+        // ---- ring termination against the offset chord (_core.pyx:359-373)
+        if (ra >= 0 && rb >= 0) {
+          __syncwarp();
+          const float4 A0 = wk[ra], A1 = wk[rb];
+          const double fx = ctl->fx, fz = ctl->fz;
+          const double ox = -0.02 * P.l_chord * nx, oz = -0.02 * P.l_chord * nz;
+          const double ax0 = A0.x, az0 = A0.y, ax1 = A1.x, az1 = A1.y;
+          const double bx0 = rx + ox, bz0 = rz + oz;
+          const double bx1 = rx - P.l_chord * fx + ox, bz1 = rz - P.l_chord * fz + oz;
+          const double d1x = ax1 - ax0, d1z = az1 - az0, d2x = bx1 - bx0, d2z = bz1 - bz0;
+          const double den = d1x * d2z - d1z * d2x;
+          bool hit = false;
+          if (den != 0.0) {
+            const double ex = bx0 - ax0, ez = bz0 - az0;
+            const double tt = (ex * d2z - ez * d2x) / den;
+            const double uu = (ex * d1z - ez * d1x) / den;
+            hit = tt >= 0.0 && tt <= 1.0 && uu >= 0.0 && uu <= 1.0;
+          }
+          if (hit) {
+            hl[nholes++] = ra;
+            hl[nholes++] = rb;
+            ra = -1;
+            rb = -1;
+          }
+        }
+        // sort holes ascending, zero their circulation, remap the ring indices
+        for (int i = 1; i < nholes; ++i) {
+          const int v = hl[i];
+          int j = i - 1;
+          while (j >= 0 && hl[j] > v) { hl[j + 1] = hl[j]; --j; }
+          hl[j + 1] = v;
+        }
+        __syncwarp();
+        if (lane < nholes) wk[hl[lane]].z = 0.f;
+        int ra2 = ra, rb2 = rb;
+        for (int h = 0; h < nholes; ++h) {
+          if (ra >= 0 && hl[h] < ra) --ra2;
+          if (rb >= 0 && hl[h] < rb) --rb2;
+        }
+        const int n_live_next = n_now - nholes;
+        // previous bound row for the next convection sweep; panels as split targets
+        for (int p = lane; p < nb; p += 32) {
+          psrc[p] = make_float4((float)bx[p], (float)bz[p], (float)(gam[p] * INV_TWO_PI), 0.f);
+          st[p] = make_float2((float)bx[p], (float)bz[p]);
+        }
+        const int xs = n_live_next > TILE ? min(XMAX, n_live_next - TILE) : 0;
+        if (lane < xs) {
+          const int r = raw_index(TILE + lane, hl, nholes);
+          st[nb + lane] = make_float2(wk[r].x, wk[r].y);
+        }
+        if (lane == 0) {
+          ctl->lev_cur = levg;
+          ctl->hp = ctl->n_prev > 0;
+          ctl->n_prev = nb;
+          ctl->pending = 1;
+          ctl->np_split = nb;
+          ctl->nx_split = xs;
+          ctl->n_raw = n_now;
+          ctl->n_live = n_live_next;
+          ctl->n_holes = nholes;
+          for (int h = 0; h < nholes; ++h) ctl->holes[h] = hl[h];
+          ctl->ring_a = ra2;
+          ctl->ring_b = rb2;
+          ctl->mcnt = min(MC, max(0, n_live_next + 3 - P.cap));
+          if (shed && t < 64) ctl->shed_mask |= 1ull << t;
+          ctl->inter += (long long)nl * (nl - 1) + (long long)n_prev * nl + (long long)nb * nl +
+                        (long long)nb * n_live_next;
+        }
+      }
+    }
+    __syncthreads();  // B4
+    if (ctl->fail) break;
+  }
+  __syncthreads();
+
+  // ---- epilogue: outputs
+  if (tid == 0) {
+    if (a.status) a.status[row] = ctl->status;
+    if (a.rc_out) a.rc_out[row] = ctl->rc;
+    if (a.shed_mask) a.shed_mask[row] = ctl->shed_mask;
+    if (a.n_final) a.n_final[row] = ctl->n_live;
+    if (a.inter) a.inter[row] = ctl->inter;
+    if (a.fw_out) { a.fw_out[3 * row] = ctl->fwx; a.fw_out[3 * row + 1] = ctl->fwz; a.fw_out[3 * row + 2] = ctl->mw; }
+    if (a.cost) {
+      // terminal cost (mppi.py:28-34): inf when failed or non-finite
+      double J = 0.0;
+      for (int i = 0; i < 7; ++i) { const double d = ctl->x[i] - a.xp[i]; J += d * a.q[i] * d; }
+      a.cost[row] = (ctl->status != 0 || !isfinite(J)) ? INFINITY : J;
+    }
+  }
+  if (a.finals && tid < 7) a.finals[(size_t)row * 7 + tid] = ctl->x[tid];
+  if (a.need_fluid && row == 0) {
+    const int cap4 = P.cap + 4;
+    const int nl = ctl->n_live, nh = ctl->n_holes;
+    for (int c = tid; c < cap4; c += NT) {
+      if (c < nl) {
+        const float4 v = wk[raw_index(c, ctl->holes, nh)];
+        a.o_wpos[2 * c] = v.x;
+        a.o_wpos[2 * c + 1] = v.y;
+        a.o_wgam[c] = (double)v.z * TWO_PI;
+        a.o_wage[c] = __float_as_int(v.w);
+      } else {
+        a.o_wpos[2 * c] = 0.0;
+        a.o_wpos[2 * c + 1] = 0.0;
+        a.o_wgam[c] = 0.0;
+        a.o_wage[c] = 0;
+      }
+    }
+    for (int p = tid; p < nb; p += NT) {
+      const bool have = p < ctl->n_prev;
+      a.o_ppos[2 * p] = have ? pxp[p] : 0.0;
+      a.o_ppos[2 * p + 1] = have ? pzp[p] : 0.0;
+      a.o_pgam[p] = have ? pgp[p] : 0.0;
+      a.o_ema[p] = ema[p];
+    }
+    if (tid == 0) {
+      a.o_scal[0] = nl;
+      a.o_scal[1] = ctl->ring_a;
+      a.o_scal[2] = ctl->ring_b;
+      a.o_scal[3] = ctl->n_prev;
+      a.o_plev[0] = ctl->lev_prev;
+    }
+  }
+}
+
+// ---- MPPI reductions -----------------------------------------------------------------
+// Partial softmax sums of one shard (mppi.py:46-59): part = {J_min, Z, S[0..T)}.
+template <int NTH>
+__global__ void __launch_bounds__(NTH) mppi_partial_kernel(const double *__restrict__ cost, int rows,
+                                                            int row_begin, const double *__restrict__ ustar,
+                                                            const double *__restrict__ noise, double sigma,
+                                                            double ulim, int T, double lambda,
+                                                            double *__restrict__ wbuf,
+                                                            double *__restrict__ part) {
+  constexpr int NW = NTH / 32;
+  extern __shared__ double sh[];  // NW * T + 2 * NW
+  double *sacc = sh;              // [NW][T]
+  double *sred = sh + NW * T;     // [2 NW]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // J_min over finite costs
+  double jm = INFINITY;
+  for (int r = tid; r < rows; r += NTH) {
+    const double J = cost[r];
+    if (isfinite(J) && J < jm) jm = J;
+  }
+  for (int o = 16; o >= 1; o >>= 1) jm = fmin(jm, __shfl_xor_sync(0xffffffffu, jm, o));
+  if (lane == 0) sred[warp] = jm;
+  __syncthreads();
+  jm = INFINITY;
+  for (int w = 0; w < NW; ++w) jm = fmin(jm, sred[w]);
+  __syncthreads();
+  const bool any = isfinite(jm);
+  // weights and normaliser
+  double z = 0.0;
+  for (int r = tid; r < rows; r += NTH) {
+    const double J = cost[r];
+    const double w = (any && isfinite(J)) ? exp(-(J - jm) / lambda) : 0.0;
+    wbuf[r] = w;
+    z += w;
+  }
+  z = warp_sum_d(z);
+  if (lane == 0) sred[NW + warp] = z;
+  __syncthreads();
+  // weighted control sums: warps stride over rows, lanes over steps
+  for (int t = lane; t < T; t += 32) sacc[warp * T + t] = 0.0;
+  for (int r = warp; r < rows; r += NW) {
+    const double w = wbuf[r];
+    if (w == 0.0) continue;
+    const int g = row_begin + r;
+    for (int t = lane; t < T; t += 32) {
+      double u = ustar[t];
+      if (g > 0) u = clampd(u + noise[(size_t)(g - 1) * T + t] * sigma, -ulim, ulim);
+      sacc[warp * T + t] += w * u;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double Z = 0.0;
+    for (int w = 0; w < NW; ++w) Z += sred[NW + w];
+    part[0] = jm;
+    part[1] = Z;
+  }
+  for (int t = tid; t < T; t += NTH) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += sacc[w * T + t];
+    part[2 + t] = s;
+  }
+}
+
+// Combine W gathered partials in rank order.
+__global__ void mppi_combine_kernel(const double *__restrict__ parts, int W, int T, double lambda,
+                                    double *__restrict__ ustar, int32_t *__restrict__ flag) {
+  const int ld = T + 2;
+  double jm = INFINITY;
+  for (int r = 0; r < W; ++r) jm = fmin(jm, parts[r * ld]);
+  if (!isfinite(jm)) {
+    if (threadIdx.x == 0 && flag) *flag = 1;
+    return;
+  }
+  double Z = 0.0;
+  for (int r = 0; r < W; ++r) {
+    const double j = parts[r * ld];
+    if (isfinite(j)) Z += parts[r * ld + 1] * exp(-(j - jm) / lambda);
+  }
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    double S = 0.0;
+    for (int r = 0; r < W; ++r) {
+      const double j = parts[r * ld];
+      if (isfinite(j)) S += parts[r * ld + 2 + t] * exp(-(j - jm) / lambda);
+    }
+    ustar[t] = S / Z;
+  }
+  if (threadIdx.x == 0 && flag) *flag = 0;
+}
+
+// FFMA-chain throughput probe (8 independent chains per thread).
+__global__ void fp32_probe_kernel(float *out, int iters, float a, float b) {
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = threadIdx.x * 1e-3f + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = fmaf(v[i], a, b);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += v[i];
+  if (s == 1.2345f) out[blockIdx.x] = s;
+}
+
+}  // namespace vpm

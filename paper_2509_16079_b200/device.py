@@ -1,0 +1,152 @@
+"""Device-resident planner plumbing: a ``vpm_plan`` handle plus torch-owned buffers.
+
+PyTorch is used only for device memory, streams and ``torch.distributed``; all
+compute is in ``libvpm_b200.so``.  :class:`DevicePlan` exposes the layer-2 C ABI
+(``include/vpm_b200.h``) on CUDA tensors:
+
+* :meth:`DevicePlan.batch` -- rollouts of an arbitrary row range of a candidate
+  set, explicit controls or MPPI sampling, optional per-row start states,
+  costs / diagnostics / trajectories (``vpm_plan_batch``);
+* :meth:`DevicePlan.mppi_partial` / :func:`mppi_combine` -- the softmax update
+  split into shard partials and a rank-ordered combine (``vpm_mppi_partial``,
+  ``vpm_mppi_combine``), the pieces the multi-GPU driver puts an NCCL
+  all-gather between (``sharding.py``);
+* :meth:`DevicePlan.mppi_iteration` -- a whole single-device iteration.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import _D, _I32, _I64, VpmBatchOut, as_f64, as_i64, check, fluid_struct, ptr
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class DevicePlan:
+    """Owns one ``vpm_plan`` (inverse boundary matrices + fluid snapshot) on a device."""
+
+    def __init__(self, iparams, fparams, device: int | None = None):
+        self.iparams = as_i64(iparams)
+        self.fparams = as_f64(fparams)
+        if device is None:
+            try:
+                torch = _torch()
+                device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+            except ImportError:
+                device = 0
+        self.device = int(device)
+        L = _lib.lib()
+        h = L.vpm_plan_create(ptr(self.iparams, _I64), ptr(self.fparams, _D), 0, 0, self.device)
+        if not h:
+            raise ValueError(f"vpm_plan_create: {_lib.last_error()}")
+        self.handle = C.c_void_p(h)
+        self.nb = int(self.iparams[0])
+        self.cap = int(self.iparams[1])
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.vpm_plan_destroy(h)
+            self.handle = None
+
+    def set_fluid(self, fluid) -> None:
+        flat = fluid.flat() if hasattr(fluid, "flat") else tuple(fluid)
+        f, keep = fluid_struct(*flat)
+        check(_lib.lib().vpm_plan_set_fluid(self.handle, C.byref(f)), "set_fluid")
+
+    # ---- rollouts -------------------------------------------------------------------
+    def batch(self, x0, T: int, *, controls=None, ustar=None, noise=None, sigma: float = 0.0,
+              row_begin: int = 0, rows: int | None = None, q=None, x_perch=None,
+              record: bool = False, diagnostics: bool = False, stream=None, out=None):
+        """Run rows [row_begin, row_begin + rows) on the device.  All tensor inputs
+        are CUDA float64 tensors; returns a dict of CUDA tensors."""
+        torch = _torch()
+        dev = x0.device
+        if rows is None:
+            rows = controls.shape[0] if controls is not None else 1
+        f64 = dict(dtype=torch.float64, device=dev)
+        o = out if out is not None else {}
+        if "status" not in o:
+            o["status"] = torch.empty(rows, dtype=torch.int64, device=dev)
+            o["finals"] = torch.empty(rows, 7, **f64)
+            if q is not None:
+                o["cost"] = torch.empty(rows, **f64)
+            if record:
+                o["trajs"] = torch.zeros(rows, T + 1, 7, **f64)
+            if diagnostics:
+                o["shed_mask"] = torch.zeros(rows, dtype=torch.int64, device=dev)
+                o["n_final"] = torch.zeros(rows, dtype=torch.int32, device=dev)
+                o["interactions"] = torch.zeros(rows, dtype=torch.int64, device=dev)
+        bo = VpmBatchOut(_p(o.get("status")), _p(o.get("finals")), _p(o.get("trajs")),
+                         _p(o.get("cost")), _p(o.get("shed_mask")), _p(o.get("n_final")),
+                         _p(o.get("interactions")))
+        stride = 7 if x0.dim() == 2 else 0
+        check(_lib.lib().vpm_plan_batch(
+            self.handle, _p(x0), stride, _p(controls), _p(ustar), _p(noise), float(sigma),
+            int(row_begin), int(row_begin + rows), int(T), _p(q), _p(x_perch), int(bool(record)),
+            C.byref(bo), _stream(stream)), "plan_batch")
+        return o
+
+    # ---- MPPI update ----------------------------------------------------------------
+    def mppi_partial(self, cost, ustar, noise, sigma: float, temperature: float,
+                     row_begin: int = 0, partial=None, stream=None):
+        torch = _torch()
+        T = int(ustar.shape[0])
+        if partial is None:
+            partial = torch.empty(T + 2, dtype=torch.float64, device=cost.device)
+        check(_lib.lib().vpm_mppi_partial(
+            self.handle, _p(cost), int(cost.shape[0]), int(row_begin), _p(ustar), _p(noise),
+            float(sigma), T, float(temperature), _p(partial), _stream(stream)), "mppi_partial")
+        return partial
+
+    def mppi_iteration(self, x0, ustar, noise, sigma: float, B_total: int, temperature: float,
+                       q, x_perch, scratch: dict, stream=None):
+        """One single-device MPPI iteration, u* updated in place."""
+        T = int(ustar.shape[0])
+        check(_lib.lib().vpm_mppi_iteration(
+            self.handle, _p(x0), _p(ustar), _p(noise), float(sigma), int(B_total), T,
+            float(temperature), _p(q), _p(x_perch), _p(scratch["cost"]), _p(scratch["partial"]),
+            _p(scratch["flag"]), 0, _stream(stream)), "mppi_iteration")
+
+    def timing(self, reset: int = 0):
+        """(average rollout-kernel ms, launches) since the last reset; reset=1 starts
+        recording CUDA events around every rollout launch, reset=-1 stops."""
+        ms = np.zeros(1)
+        n = np.zeros(1, dtype=np.int64)
+        check(_lib.lib().vpm_plan_timing(self.handle, int(reset), ptr(ms, _D), ptr(n, _I64)),
+              "plan_timing")
+        return float(ms[0]), int(n[0])
+
+
+def mppi_combine(partials, temperature: float, ustar, flag=None, stream=None):
+    """Combine (W, T+2) gathered shard partials in rank order into ``ustar``."""
+    W, ld = int(partials.shape[0]), int(partials.shape[1])
+    check(_lib.lib().vpm_mppi_combine(_p(partials), W, ld - 2, float(temperature), _p(ustar),
+                                      _p(flag), _stream(stream)), "mppi_combine")
+
+
+def launch_shape(cap: int, nb: int):
+    t, r, s = (np.zeros(1, np.int32) for _ in range(3))
+    _lib.lib().vpm_launch_shape(int(cap), int(nb), ptr(t, _I32), ptr(r, _I32), ptr(s, _I32))
+    return int(t[0]), int(r[0]), int(s[0])
+
+
+def fp32_peak_gflops(iters: int = 4096) -> float:
+    return float(_lib.lib().vpm_fp32_peak_probe(int(iters)))

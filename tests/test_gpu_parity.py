@@ -1,0 +1,312 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's golden
+vectors and the FP64 CPU oracle on identical inputs and identical noise.
+
+Tolerances (stated, FP32 Biot-Savart vs FP64 reference):
+  * discrete decisions -- status, shed steps (bitmask), final wake size -- exact,
+    except on rollouts whose oracle-recorded gate or ring-termination margin is
+    below GATE_DELTA / RING_DELTA (near-ties, counted and reported, never hidden);
+  * states, costs, u*: |gpu - ref| <= RTOL * max(1, |ref|) with RTOL = 1e-4.
+"""
+import numpy as np
+import pytest
+
+from conftest import flat_of, golden
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4
+GATE_DELTA = 1e-4   # rad
+RING_DELTA = 1e-4   # intersection-parameter margin
+X0 = np.array([0.0, 0.0, 0.3, 0.0, 7.0, 0.0, 0.0])
+
+
+def close(a, b, rtol=RTOL):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.abs(a - b) <= rtol * np.maximum(1.0, np.abs(b))
+
+
+def assert_close(a, b, rtol=RTOL, what=""):
+    ok = close(a, b, rtol)
+    if not ok.all():
+        i = np.unravel_index(np.argmax(np.abs(np.asarray(a) - np.asarray(b))), np.shape(a))
+        raise AssertionError(f"{what}: {int((~ok).sum())} entries off, worst at {i}: "
+                             f"{np.asarray(a)[i]} vs {np.asarray(b)[i]}")
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    torch.cuda.set_device(0)
+    return torch
+
+
+def engine_for(iparams, fparams):
+    from paper_2509_16079_b200 import config, rollout
+    v = config.VpmConfig(particle_cap=int(iparams[1]))
+    e = rollout.Engine(v, config.GliderParams())
+    np.testing.assert_array_equal(e.fparams, fparams)
+    return e
+
+
+def fluid_from(g, cap):
+    from paper_2509_16079_b200 import config, vpm
+    f = vpm.FluidState.empty(config.VpmConfig(particle_cap=cap))
+    (wp, wg, wa, n, ra, rb, pp, pg, m, pl, em) = flat_of(g)
+    f.wake_pos[:n], f.wake_gamma[:n], f.wake_age[:n] = wp[:n], wg[:n], wa[:n]
+    f.n_wake, f.ring_a, f.ring_b = n, ra, rb
+    f.prev_pos[:m], f.prev_gamma[:m], f.n_prev, f.prev_lev_gamma = pp[:m], pg[:m], m, pl
+    f.unsteady_ema[:] = em
+    return f
+
+
+# ------------------------------------------------------------------ golden vectors
+def test_c1_step_sequence(torch_cuda):
+    g = golden("c1_steps.npz")
+    eng = engine_for(g["iparams"], g["fparams"])
+    from paper_2509_16079_b200 import vpm
+    fl = vpm.FluidState.empty(eng.cfg)
+    x = X0.copy()
+    for t in range(50):
+        ok, x, fl, fw = eng.step(x, -15.0, fl)
+        assert ok
+        assert fl.n_wake == g["n_wake_steps"][t], t
+        assert_close(x, g["states"][t + 1], what=f"state step {t}")
+        assert_close(fw, g["fw"][t], rtol=1e-3, what=f"fw step {t}")
+    n = int(g["n_wake"])
+    assert fl.n_wake == n == 96
+    np.testing.assert_array_equal(fl.wake_age[:n], g["wake_age"][:n])
+    assert_close(fl.wake_pos[:n], g["wake_pos"][:n], what="wake_pos")
+    assert_close(fl.wake_gamma[:n], g["wake_gamma"][:n], rtol=1e-3, what="wake_gamma")
+
+
+def test_c1_rollout_and_fluid(torch_cuda):
+    g = golden("c1_steps.npz")
+    eng = engine_for(g["iparams"], g["fparams"])
+    from paper_2509_16079_b200 import vpm
+    rc, traj, fl = eng.rollout(X0, np.full(50, -15.0), vpm.FluidState.empty(eng.cfg), record=True)
+    assert rc == 0 and fl.n_wake == 96
+    assert_close(traj, g["states"], what="traj")
+    np.testing.assert_array_equal(fl.wake_age[:96], g["wake_age"][:96])
+
+
+def test_batch_ring_golden(torch_cuda):
+    g = golden("batch_ring.npz")
+    eng = engine_for(g["iparams"], g["fparams"])
+    from paper_2509_16079_b200 import rollout
+    res = eng.batch(rollout.RolloutRequest(x0=X0, fluid=fluid_from(g, 128), controls=g["controls"],
+                                           record=True))
+    np.testing.assert_array_equal(res.status, g["status"])
+    assert_close(res.trajectories, g["trajs"], what="trajs")
+
+
+def test_fluid_step_matches_oracle(torch_cuda, oracle_core):
+    sc = golden("scenario_C3.npz")
+    eng = engine_for(sc["iparams"], sc["fparams"])
+    fl = fluid_from(sc, 256)
+    x = X0.copy()
+    for k in range(3):
+        fl_g, fw, mw = eng.fluid_step(x, fl)
+        rc, _, fw_o, mw_o, flat_o = oracle_core.step(x, 0.0, *fl.flat(), eng.iparams, eng.fparams, False)
+        assert rc == 0 and fl_g.n_wake == flat_o[3] and (fl_g.ring_a, fl_g.ring_b) == flat_o[4:6]
+        n = fl_g.n_wake
+        np.testing.assert_array_equal(fl_g.wake_age[:n], flat_o[2][:n])
+        assert_close(fl_g.wake_pos[:n], flat_o[0][:n], what="pos")
+        assert_close(fw, fw_o, rtol=1e-3, what="fw")
+        fl = fl_g
+        x[0] += 0.07
+
+
+def test_mppi_C2_golden(torch_cuda):
+    from paper_2509_16079_b200 import config, mppi
+    g = golden("mppi_C2.npz")
+    sc = golden("scenario_C2.npz")
+    eng = engine_for(sc["iparams"], sc["fparams"])
+    mcfg = config.MppiConfig(batch=256, iterations=3, horizon=50)
+    u = mppi.optimize(sc["x0"], fluid_from(sc, 60), sc["warm"], mcfg, eng,
+                      np.random.default_rng(int(g["seed"])))
+    assert_close(u, g["u_star"], rtol=1e-3, what="u*")
+
+
+def _device_iteration(torch, sc, K, seed, diagnostics=True):
+    """One MPPI candidate batch through the device plan (C ABI layer 2)."""
+    from paper_2509_16079_b200.device import DevicePlan
+    plan = DevicePlan(sc["iparams"], sc["fparams"])
+    plan.set_fluid(flat_of(sc))
+    noise = np.random.default_rng(seed).normal(0.0, 1.0, (1, K, 50))
+    dev = torch.device("cuda")
+    f64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev)
+    q = f64([10, 10, 1, 0, 0.2, 0.2, 0.2])
+    xp = f64([3.5, 0, np.pi / 4, 0, 0.5, -0.5, 0])
+    out = plan.batch(f64(sc["x0"]), 50, ustar=f64(sc["warm"]), noise=f64(noise[0]), sigma=2.0,
+                     rows=K + 1, q=q, x_perch=xp, diagnostics=diagnostics)
+    torch.cuda.synchronize()
+    return plan, noise, {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def _oracle_iteration(oracle_core, sc, noise):
+    from oracle import planner
+    cand = planner.candidates(sc["warm"], noise[0], 2.0, 15.0)
+    d = oracle_core.batch_rollout_diag(sc["x0"], cand, *flat_of(sc), sc["iparams"], sc["fparams"])
+    d["cost"] = planner.terminal_costs(d["finals"], d["status"], [10, 10, 1, 0, 0.2, 0.2, 0.2],
+                                       [3.5, 0, np.pi / 4, 0, 0.5, -0.5, 0])
+    d["cand"] = cand
+    return d
+
+
+@pytest.mark.parametrize("name,K,seed", [("scenario_C2.npz", 256, 11), ("scenario_C3.npz", 128, 12),
+                                         ("scenario_C4.npz", 64, 13)])
+def test_device_batch_vs_oracle_margin_aware(torch_cuda, oracle_core, name, K, seed):
+    sc = golden(name)
+    _, noise, gpu = _device_iteration(torch_cuda, sc, K, seed)
+    ref = _oracle_iteration(oracle_core, sc, noise)
+    near = (ref["gate_margin"] < GATE_DELTA) | (ref["ring_margin"] < RING_DELTA)
+    clean = ~near
+    print(f"{name}: {int(near.sum())} near-tie rollouts of {K + 1}")
+    np.testing.assert_array_equal(gpu["status"][clean], ref["status"][clean])
+    np.testing.assert_array_equal(gpu["shed_mask"][clean].astype(np.uint64), ref["shed_mask"][clean])
+    np.testing.assert_array_equal(gpu["n_final"][clean], ref["n_final"][clean])
+    ok = clean & (ref["status"] == 0)
+    assert_close(gpu["finals"][ok], ref["finals"][ok], what="finals")
+    assert_close(gpu["cost"][ok], ref["cost"][ok], what="cost")
+    assert near.mean() < 0.05
+
+
+def test_mppi_update_vs_oracle(torch_cuda, oracle_core):
+    """Softmax weights and u* from the device partial + combine kernels."""
+    import torch
+    from oracle import planner
+    from paper_2509_16079_b200.device import mppi_combine
+    sc = golden("scenario_C3.npz")
+    K = 128
+    plan, noise, gpu = _device_iteration(torch, sc, K, 21, diagnostics=False)
+    ref = _oracle_iteration(oracle_core, sc, noise)
+    dev = torch.device("cuda")
+    cost = torch.as_tensor(gpu["cost"], device=dev)
+    us = torch.as_tensor(np.ascontiguousarray(sc["warm"]), device=dev)
+    nz = torch.as_tensor(noise[0], device=dev)
+    part = plan.mppi_partial(cost, us, nz, 2.0, 0.05)
+    new = torch.empty_like(us)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    mppi_combine(part.view(1, -1), 0.05, new, flag)
+    torch.cuda.synchronize()
+    assert flag.item() == 0
+    u_ref = planner.weighted_mean(ref["cand"], ref["cost"], 0.05)
+    # same costs in -> FP64 update agrees to rounding
+    u_same = planner.weighted_mean(ref["cand"], gpu["cost"], 0.05)
+    np.testing.assert_allclose(new.cpu().numpy(), u_same, rtol=1e-10, atol=1e-12)
+    assert_close(new.cpu().numpy(), u_ref, rtol=1e-3, what="u*")
+
+
+def test_policy_C2_golden(torch_cuda):
+    from paper_2509_16079_b200 import config, policy
+    g = golden("policy_C2.npz")
+    sc = golden("scenario_C2.npz")
+    eng = engine_for(sc["iparams"], sc["fparams"])
+    nom = policy.NominalTrajectory(states=g["nominal_states"], inputs=g["nominal_inputs"], dt=0.01)
+    states, inputs, ok = policy.perturbed_rollouts(nom, fluid_from(sc, 60), config.SynthesisConfig(),
+                                                   eng, np.random.default_rng(int(g["seed"])))
+    np.testing.assert_array_equal(ok, g["cloud_ok"])
+    assert_close(states[ok], g["cloud_states"][ok], what="cloud")
+    pol = policy.build_policy(nom, fluid_from(sc, 60), config.SynthesisConfig(), eng,
+                              np.random.default_rng(int(g["seed"])))
+    assert_close(pol.gains, g["gains"], rtol=2e-2, what="gains")
+
+
+# ------------------------------------------------------------------ full-size properties
+def test_c4_full_batch_properties(torch_cuda, oracle_core):
+    """K=4096, H=50, N=512 + ring: deterministic, row-independent (batch ==
+    sub-batch), finite, and a random subset matches the oracle."""
+    torch = torch_cuda
+    sc = golden("scenario_C4.npz")
+    K = 4096
+    plan, noise, a = _device_iteration(torch, sc, K, 5)
+    _, _, b = _device_iteration(torch, sc, K, 5)
+    for k in ("status", "finals", "cost", "shed_mask", "n_final"):
+        np.testing.assert_array_equal(a[k], b[k])
+    assert np.all(a["n_final"] <= 512) and np.all(a["n_final"] >= 500)
+    # a 33-row slice computed alone is bitwise identical to the same rows of the full batch
+    from paper_2509_16079_b200.device import DevicePlan
+    dev = torch.device("cuda")
+    f64 = lambda v: torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64), device=dev)
+    q = f64([10, 10, 1, 0, 0.2, 0.2, 0.2])
+    xp = f64([3.5, 0, np.pi / 4, 0, 0.5, -0.5, 0])
+    sub = plan.batch(f64(sc["x0"]), 50, ustar=f64(sc["warm"]), noise=f64(noise[0]), sigma=2.0,
+                     row_begin=2000, rows=33, q=q, x_perch=xp)
+    np.testing.assert_array_equal(sub["finals"].cpu().numpy(), a["finals"][2000:2033])
+    # oracle on 24 random rows
+    rows = np.random.default_rng(0).choice(K + 1, 24, replace=False)
+    from oracle import planner
+    cand = planner.candidates(sc["warm"], noise[0], 2.0, 15.0)[rows]
+    d = oracle_core.batch_rollout_diag(sc["x0"], cand, *flat_of(sc), sc["iparams"], sc["fparams"])
+    clean = (d["gate_margin"] >= GATE_DELTA) & (d["ring_margin"] >= RING_DELTA)
+    np.testing.assert_array_equal(a["status"][rows][clean], d["status"][clean])
+    np.testing.assert_array_equal(a["shed_mask"][rows][clean].astype(np.uint64), d["shed_mask"][clean])
+    ok = clean & (d["status"] == 0)
+    assert_close(a["finals"][rows][ok], d["finals"][ok], what="finals")
+
+
+# ------------------------------------------------------------------ edge cases
+def test_zero_horizon_and_empty_batch(torch_cuda):
+    from paper_2509_16079_b200 import config, rollout, vpm
+    eng = rollout.Engine(config.VpmConfig(), config.GliderParams())
+    fl = vpm.FluidState.empty(eng.cfg)
+    rc, traj, fo = eng.rollout(X0, np.zeros(0), fl, record=True)
+    assert rc == 0 and traj.shape == (1, 7) and np.array_equal(traj[0], X0) and fo.n_wake == 0
+    res = eng.batch(rollout.RolloutRequest(x0=X0, fluid=fl, controls=np.zeros((0, 5))))
+    assert res.status.shape == (0,)
+
+
+@pytest.mark.parametrize("nb,cap", [(4, 4), (10, 8), (17, 40), (33, 100), (10, 300)])
+def test_odd_configs_vs_oracle(torch_cuda, oracle_core, nb, cap):
+    """Small caps (merging every step, ring protected), nb beyond a warp, tile overflow."""
+    from paper_2509_16079_b200 import config, rollout, vpm
+    v = config.VpmConfig(n_bound=nb, particle_cap=cap)
+    eng = rollout.Engine(v, config.GliderParams())
+    fl = vpm.FluidState.empty(v)
+    fl = vpm.inject_ring(fl, vpm.RingDisturbance.from_speed([0.8, -0.05], 7.5, 0.28, 0.02, -1.0))
+    rng = np.random.default_rng(nb * 1000 + cap)
+    ctrl = np.clip(-8.0 + 4.0 * rng.normal(0, 1, (16, 40)), -15, 15)
+    res = eng.batch(rollout.RolloutRequest(x0=X0, fluid=fl, controls=ctrl, record=True))
+    d = oracle_core.batch_rollout_diag(X0, ctrl, *fl.flat(), eng.iparams, eng.fparams, record=True)
+    clean = (d["gate_margin"] >= GATE_DELTA) & (d["ring_margin"] >= RING_DELTA)
+    np.testing.assert_array_equal(res.status[clean], d["status"][clean])
+    ok = clean & (d["status"] == 0)
+    assert_close(res.trajectories[ok], d["trajs"][ok], rtol=1e-3, what="trajs")
+
+
+def test_overfull_snapshot_and_reversed_flow(torch_cuda, oracle_core):
+    """n_wake = cap + 4 at fork (overflow targets + 4-6 merges in one step) and a
+    tail-first plate (|aoa| > 90 deg: reversed-flow rows and edge roles)."""
+    from paper_2509_16079_b200 import config, rollout, vpm
+    sc = golden("scenario_C3.npz")
+    v = config.VpmConfig(particle_cap=128)  # register tile 64 x 2 = 128 < 132 particles
+    eng = rollout.Engine(v, config.GliderParams())
+    fl = vpm.FluidState.empty(v)
+    keep = list(range(130)) + [int(sc["ring_a"]), int(sc["ring_b"])]
+    n = len(keep)  # cap + 4
+    fl.wake_pos[:n], fl.wake_gamma[:n], fl.wake_age[:n] = (sc["wake_pos"][keep], sc["wake_gamma"][keep],
+                                                           sc["wake_age"][keep])
+    fl.n_wake, fl.ring_a, fl.ring_b = n, 130, 131
+    for x0 in (X0, np.array([0.0, 0.0, 0.2, 0.0, -6.0, 0.5, 0.0])):
+        ctrl = np.full((3, 20), -4.0)
+        ctrl[1] = 6.0
+        ctrl[2] = np.linspace(-15, 15, 20)
+        res = eng.batch(rollout.RolloutRequest(x0=x0, fluid=fl, controls=ctrl, record=True))
+        d = oracle_core.batch_rollout_diag(x0, ctrl, *fl.flat(), eng.iparams, eng.fparams, record=True)
+        np.testing.assert_array_equal(res.status, d["status"])
+        ok = d["status"] == 0
+        assert_close(res.trajectories[ok], d["trajs"][ok], rtol=1e-3, what="trajs")
+
+
+def test_envelope_blowup_status(torch_cuda, oracle_core):
+    from paper_2509_16079_b200 import config, rollout, vpm
+    v = config.VpmConfig(particle_cap=60)
+    eng = rollout.Engine(v, config.GliderParams())
+    fl = vpm.FluidState.empty(v)
+    x0 = np.array([0.0, 0.0, 0.0, 0.0, 7.0, 0.0, 290.0])  # spins past |omega| > 300
+    ctrl = np.full((2, 10), 15.0)
+    res = eng.batch(rollout.RolloutRequest(x0=x0, fluid=fl, controls=ctrl))
+    d = oracle_core.batch_rollout_diag(x0, ctrl, *fl.flat(), eng.iparams, eng.fparams)
+    np.testing.assert_array_equal(res.status, d["status"])
+    assert (res.status > 0).all()
