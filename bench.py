@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""bench.py -- MPPI replanning iteration of the VPM perching planner on B200.
+
+Workload (BASELINE.json config C4): one MPPI iteration = K=4096 sampled control
+sequences + the incumbent (B=4097 rollouts), H=50 coupled glider + vortex-wake
+steps each, particle cap N=512 on a prefilled synthetic wake (510 particles,
+reference-generated fixture tests/golden/scenario_C4.npz) plus the planarised
+ring-vortex pair; x0=[0,0,0.3,0,7,0,0], warm start -6 rad/s, sigma=2, lambda=0.05,
+noise = numpy default_rng(seed).normal(0, 1, (K, H)) per iteration.
+
+  value        rollouts/s of the whole job (B x steps / device time, max over ranks)
+  ms_per_step  MPPI iteration latency (device, CUDA events on the launch stream)
+  e2e          same metric through the C ABI with host buffers (vpm_plan_set_fluid +
+               vpm_mppi_optimize_host: H2D of snapshot/noise/u*, D2H of u*)
+  roofline     rollout kernel vs the FP32 CUDA-core peak (12 flop per directed
+               regularised Biot-Savart interaction, counted exactly by the kernel)
+
+``--impl reference`` times the reference's own compiled CPU core
+(oracle/_ref, Cython + OpenMP FP64, all host threads) on a bounded sample of the
+same workload, driven by the numpy restatement of mppi.py.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+K_SAMPLES, HORIZON, CAP = 4096, 50, 512
+SIGMA, LAMBDA = 2.0, 0.05
+Q = [10.0, 10.0, 1.0, 0.0, 0.2, 0.2, 0.2]
+XPERCH = [3.5, 0.0, np.pi / 4.0, 0.0, 0.5, -0.5, 0.0]
+FP32_SPEC_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4, SMs x lanes x FMA x max clock
+METRIC = "MPPI iteration rollouts/s (K=4096, H=50, N<=512 + ring)"
+CONFIG = {"workload": "C4: MPPI perching + ring vortex, K=4096 (+incumbent), H=50, N<=512",
+          "K": K_SAMPLES, "H": HORIZON, "particle_cap": CAP, "n_bound": 10,
+          "scenario": "tests/golden/scenario_C4.npz (reference-generated prefilled wake + ring)",
+          "l2": "flushed (256 MiB write) before every timed iteration"}
+
+
+def load_scenario():
+    with np.load(os.path.join(ROOT, "tests", "golden", "scenario_C4.npz")) as z:
+        sc = {k: z[k] for k in z.files}
+    flat = (sc["wake_pos"], sc["wake_gamma"], sc["wake_age"], int(sc["n_wake"]), int(sc["ring_a"]),
+            int(sc["ring_b"]), sc["prev_pos"], sc["prev_gamma"], int(sc["n_prev"]),
+            float(sc["prev_lev"]), sc["ema"])
+    return sc, flat
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def read_traffic():
+    """DRAM bytes per rollout-kernel launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "rollout_kernel_ncu.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    return None
+
+
+# ------------------------------------------------------------------------------ CPU arm
+def reference_core():
+    from oracle import refcore
+    mod = refcore.load()
+    if mod is not None:
+        return mod, "reference"
+    from oracle import core
+    core.build()
+    return core, "port"
+
+
+def time_cpu_sample(core, sc, flat, noise, rows):
+    """Run ``rows`` candidate rows of the C4 iteration on the host; returns seconds."""
+    from oracle import planner
+    cand = planner.candidates(np.full(HORIZON, -6.0), noise[: rows - 1], SIGMA, 15.0)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    status, finals, _ = core.batch_rollout(sc["x0"], np.ascontiguousarray(cand), *flat, sc["iparams"],
+                                           sc["fparams"], False, threads)
+    J = planner.terminal_costs(finals, status, Q, XPERCH)
+    planner.weighted_mean(cand, J, LAMBDA)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(sc, flat, target_s=12.0):
+    core, kind = reference_core()
+    noise = np.random.default_rng(1234).normal(0.0, 1.0, (K_SAMPLES, HORIZON))
+    threads = os.cpu_count() or 1
+    probe = max(2, min(K_SAMPLES + 1, threads * 2))
+    dt = time_cpu_sample(core, sc, flat, noise, probe)
+    rows = int(min(K_SAMPLES + 1, max(probe, probe * target_s / max(dt, 1e-6))))
+    rows = max(threads, (rows // threads) * threads) if rows < K_SAMPLES + 1 else rows
+    dt = time_cpu_sample(core, sc, flat, noise, rows)
+    return {"value": rows / dt, "unit": "rollouts/s", "cores": threads, "kind": kind,
+            "sample": f"{rows} of the {K_SAMPLES + 1} C4 candidate rollouts (H=50, N=512 + ring), "
+                      f"FP64, {threads} OpenMP threads, {dt:.1f} s; full iteration would take "
+                      f"{(K_SAMPLES + 1) / (rows / dt):.1f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sc, flat = load_scenario()
+    core, kind = reference_core()
+    noise = np.random.default_rng(1234).normal(0.0, 1.0, (K_SAMPLES, HORIZON))
+    threads = os.cpu_count() or 1
+    rows = max(threads * 2, 16)
+    for _ in range(max(args.warmup, 1)):
+        dt = time_cpu_sample(core, sc, flat, noise, rows)
+    # size each timed step at about 4 s so --steps K --warmup W stays within minutes
+    rows = int(min(K_SAMPLES + 1, max(rows, rows * 4.0 / max(dt, 1e-6))))
+    times = [time_cpu_sample(core, sc, flat, noise, rows) for _ in range(args.steps)]
+    tot = sum(times)
+    value = rows * args.steps / tot
+    line = {"metric": METRIC, "value": value, "unit": "rollouts/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * (K_SAMPLES + 1) / value, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": CONFIG,
+            "cpu_baseline": {"value": value, "unit": "rollouts/s", "cores": threads, "kind": kind,
+                             "sample": f"{rows} of {K_SAMPLES + 1} C4 rollouts per step"},
+            "e2e": {"value": value, "unit": "rollouts/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2509_16079_b200 import _lib
+    from paper_2509_16079_b200.device import DevicePlan, fp32_peak_gflops, launch_shape
+    from paper_2509_16079_b200.sharding import ShardedMppi
+
+    sc, flat = load_scenario()
+    dev = torch.device("cuda", local)
+    f64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev)
+    B = K_SAMPLES + 1
+    plan = DevicePlan(sc["iparams"], sc["fparams"], device=local)
+    plan.set_fluid(flat)
+    nsteps = args.warmup + args.steps
+    noise_all = [f64(np.random.default_rng(100 + i).normal(0.0, 1.0, (K_SAMPLES, HORIZON)))
+                 for i in range(nsteps)]
+    warm = f64(np.full(HORIZON, -6.0))
+    mp = ShardedMppi(plan, f64(sc["x0"]), warm, noise_all[0], B=B, sigma=SIGMA, temperature=LAMBDA,
+                     q=f64(Q), x_perch=f64(XPERCH), rank=rank, world=world)
+    mp.out["interactions"] = torch.zeros(mp.end - mp.begin, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    for i in range(args.warmup):
+        mp.set_noise(noise_all[i])
+        mp.iteration()
+    torch.cuda.synchronize()
+    mp.check()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    inter_total = 0
+    plan.timing(reset=1)  # start CUDA-event timing of every rollout launch
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.zero_()
+            mp.set_noise(noise_all[args.warmup + s])
+            ev[s][0].record(stream)
+            mp.iteration()
+            ev[s][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    kern_ms, launches = plan.timing(reset=-1)
+    mp.check()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(sum(step_ms))
+    inter_total = int(mp.out["interactions"].sum().item())  # last iteration's count
+    stats = torch.tensor([tot_ms, kern_ms, float(inter_total)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = stats.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = stats.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        tot_ms, kern_ms_max, inter_all = float(mx[0]), float(mx[1]), float(sm[2])
+    else:
+        kern_ms_max, inter_all = kern_ms, float(inter_total)
+    ms_per_step = tot_ms / args.steps
+    value = B * args.steps / (tot_ms * 1e-3)
+
+    # ---- end to end through the C ABI with host buffers (rank-local, 1 GPU)
+    e2e = None
+    if world == 1:
+        import ctypes as C
+        from paper_2509_16079_b200._lib import _D, VpmFluid, check, fluid_struct, ptr
+        pin = torch.empty((args.steps, K_SAMPLES, HORIZON), dtype=torch.float64).pin_memory()
+        pin_np = pin.numpy()
+        for s in range(args.steps):
+            pin_np[s] = noise_all[args.warmup + s].cpu().numpy()
+        u_host = torch.empty(HORIZON, dtype=torch.float64).pin_memory().numpy()
+        x0h = np.ascontiguousarray(sc["x0"])
+        qh, xph = np.asarray(Q, float), np.asarray(XPERCH, float)
+        L = _lib.lib()
+        fstruct, keep = fluid_struct(*flat)
+
+        def one(s):
+            u_host[:] = -6.0
+            check(L.vpm_plan_set_fluid(plan.handle, C.byref(fstruct)), "set_fluid")
+            check(L.vpm_mppi_optimize_host(plan.handle, ptr(x0h, _D), ptr(u_host, _D),
+                                           ptr(pin_np[s], _D), 1, K_SAMPLES, HORIZON, SIGMA, LAMBDA,
+                                           ptr(qh, _D), ptr(xph, _D)), "optimize_host")
+
+        one(0)
+        t0 = time.perf_counter()
+        for s in range(args.steps):
+            one(s)
+        e2e_s = time.perf_counter() - t0
+        h2d = K_SAMPLES * HORIZON * 8 + HORIZON * 8 + 3 * 7 * 8 + int(sc["n_wake"]) * 32 + 10 * 32
+        e2e = {"value": B * args.steps / e2e_s, "unit": "rollouts/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": HORIZON * 8 + 4, "ms_per_step": 1e3 * e2e_s / args.steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    nt, r, smem = launch_shape(CAP, 10)
+    peak_meas = fp32_peak_gflops() / 1e3
+    peak = max(peak_meas, FP32_SPEC_TFLOPS)
+    flops_per_launch = 12.0 * inter_all / max(world, 1)
+    achieved = flops_per_launch / (kern_ms_max * 1e-3) / 1e12 if kern_ms_max > 0 else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "rollouts/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": dict(CONFIG, parallelism=f"rollout rows sharded over {world} GPU(s), "
+                                           "1 all_gather of W x (H+2) f64 per iteration"),
+        "latency_ms": ms_per_step,
+        "biot_savart_gflops": 12.0 * inter_all / (kern_ms_max * 1e-3) / 1e9 if kern_ms_max > 0 else None,
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": read_traffic(),
+                     "kernel": f"rollout_kernel<{nt},{r}> (one CTA per rollout, {smem} B smem)",
+                     "flop_per_launch": flops_per_launch,
+                     "kernel_ms": kern_ms_max,
+                     "peak_source": f"max(FFMA probe {peak_meas:.1f}, spec 148x128x2x1.965GHz "
+                                    f"{FP32_SPEC_TFLOPS:.1f}) TFLOP/s; MEASURED_PEAKS.json has no FP32 entry"},
+        "gpu_launches": ShardedMppi.kernels_per_iteration * args.steps,
+        "clocks": clk.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(sc, flat)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -169,8 +169,9 @@ int vpm_mppi_optimize_host(vpm_plan *p, const double *x0, double *u_star, const 
  * the last reset, timed with CUDA events on the launch stream. */
 int vpm_plan_timing(vpm_plan *p, int reset, double *avg_ms, int64_t *launches);
 
-/* FP32 FFMA throughput microbenchmark (GFLOP/s) on the current device. */
-double vpm_fp32_peak_probe(int iters);
+/* Pipe throughput microbenchmark on the current device: mode 0 FFMA (GFLOP/s),
+ * 1 packed FFMA2 (GFLOP/s), 2 MUFU.RSQ (G ops/s). */
+double vpm_fp32_peak_probe(int iters, int mode);
 
 /* Host-only: the inverses of the three pose-invariant boundary systems the solve
  * uses (attached nb x nb, shedding forward, shedding reversed; (nb+2)^2 doubles

@@ -500,19 +500,24 @@ int vpm_plan_timing(vpm_plan *p, int reset, double *avg_ms, int64_t *launches) {
   return VPM_OK;
 }
 
-double vpm_fp32_peak_probe(int iters) {
+double vpm_fp32_peak_probe(int iters, int mode) {
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1.0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int blocks = sms * 8, threads = 256;
   float *d = nullptr;
   if (cudaMalloc(&d, blocks * sizeof(float)) != cudaSuccess) return -1.0;
+  auto run = [&](int it) {
+    if (mode == 1) vpm::fp32_probe_kernel<1><<<blocks, threads>>>(d, it, 0.9999f, 1e-4f);
+    else if (mode == 2) vpm::fp32_probe_kernel<2><<<blocks, threads>>>(d, it, 0.9999f, 1e-4f);
+    else vpm::fp32_probe_kernel<0><<<blocks, threads>>>(d, it, 0.9999f, 1e-4f);
+  };
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  vpm::fp32_probe_kernel<<<blocks, threads>>>(d, iters / 4, 0.9999f, 1e-4f);  // warm-up
+  run(iters / 4);  // warm-up
   cudaEventRecord(a);
-  vpm::fp32_probe_kernel<<<blocks, threads>>>(d, iters, 0.9999f, 1e-4f);
+  run(iters);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms = 0.f;
@@ -520,8 +525,10 @@ double vpm_fp32_peak_probe(int iters) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(d);
-  const double flops = 2.0 * 8.0 * (double)iters * blocks * threads;
-  return ms > 0.f ? flops / (ms * 1e-3) / 1e9 : -1.0;
+  // GFLOP/s for FFMA (2/lane-op) and FFMA2 (4/lane-op); G ops/s for MUFU
+  const double per = mode == 1 ? 4.0 : (mode == 2 ? 1.0 : 2.0);
+  const double work = per * 8.0 * (double)iters * blocks * threads;
+  return ms > 0.f ? work / (ms * 1e-3) / 1e9 : -1.0;
 }
 
 int vpm_boundary_inverse(const int64_t *iparams, const double *fparams, double *out) {

@@ -909,18 +909,42 @@ __global__ void mppi_combine_kernel(const double *__restrict__ parts, int W, int
   if (threadIdx.x == 0 && flag) *flag = 0;
 }
 
-// FFMA-chain throughput probe (8 independent chains per thread).
+// Pipe throughput probes, 8 independent chains per thread.
+//   MODE 0: FFMA (2 flop / lane / op)   MODE 1: FFMA2 packed f32x2 (4 flop / lane / op)
+//   MODE 2: MUFU.RSQ (1 op / lane)
+template <int MODE>
 __global__ void fp32_probe_kernel(float *out, int iters, float a, float b) {
-  float v[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = threadIdx.x * 1e-3f + i;
-  for (int it = 0; it < iters; ++it) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = fmaf(v[i], a, b);
-  }
   float s = 0.f;
+  if constexpr (MODE == 1) {
+    unsigned long long v[8], A, Bv;
+    const float2 af = make_float2(a, a), bf = make_float2(b, b);
+    A = *reinterpret_cast<const unsigned long long *>(&af);
+    Bv = *reinterpret_cast<const unsigned long long *>(&bf);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) s += v[i];
+    for (int i = 0; i < 8; ++i) {
+      const float2 t = make_float2(threadIdx.x * 1e-3f + i, 0.5f * i);
+      v[i] = *reinterpret_cast<const unsigned long long *>(&t);
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(v[i]) : "l"(A), "l"(Bv));
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float2 t = *reinterpret_cast<const float2 *>(&v[i]);
+      s += t.x + t.y;
+    }
+  } else {
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = 1.0f + threadIdx.x * 1e-3f + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = MODE == 0 ? fmaf(v[i], a, b) : rsqrt_mufu(v[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += v[i];
+  }
   if (s == 1.2345f) out[blockIdx.x] = s;
 }
 

@@ -148,5 +148,6 @@ def launch_shape(cap: int, nb: int):
     return int(t[0]), int(r[0]), int(s[0])
 
 
-def fp32_peak_gflops(iters: int = 4096) -> float:
-    return float(_lib.lib().vpm_fp32_peak_probe(int(iters)))
+def fp32_peak_gflops(iters: int = 4096, mode: int = 0) -> float:
+    """Measured pipe throughput: mode 0 FFMA GFLOP/s, 1 FFMA2 GFLOP/s, 2 MUFU.RSQ G ops/s."""
+    return float(_lib.lib().vpm_fp32_peak_probe(int(iters), int(mode)))
