@@ -262,27 +262,36 @@ def run_ours(args):
         L = _lib.lib()
         fstruct, keep = fluid_struct(*flat)
 
+        split = [0.0, 0.0]
+
         def one(s):
             u_host[:] = -6.0
+            t_a = time.perf_counter()
             check(L.vpm_plan_set_fluid(plan.handle, C.byref(fstruct)), "set_fluid")
+            t_b = time.perf_counter()
             check(L.vpm_mppi_optimize_host(plan.handle, ptr(x0h, _D), ptr(u_host, _D),
                                            ptr(pin_np[s], _D), 1, K_SAMPLES, HORIZON, SIGMA, LAMBDA,
                                            ptr(qh, _D), ptr(xph, _D)), "optimize_host")
+            split[0] += t_b - t_a
+            split[1] += time.perf_counter() - t_b
 
         one(0)
+        split[:] = [0.0, 0.0]
         t0 = time.perf_counter()
         for s in range(args.steps):
             one(s)
         e2e_s = time.perf_counter() - t0
         h2d = K_SAMPLES * HORIZON * 8 + HORIZON * 8 + 3 * 7 * 8 + int(sc["n_wake"]) * 32 + 10 * 32
         e2e = {"value": B * args.steps / e2e_s, "unit": "rollouts/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": HORIZON * 8 + 4, "ms_per_step": 1e3 * e2e_s / args.steps}
+               "d2h_bytes_per_step": HORIZON * 8 + 4, "ms_per_step": 1e3 * e2e_s / args.steps,
+               "set_fluid_ms": 1e3 * split[0] / args.steps,
+               "optimize_ms": 1e3 * split[1] / args.steps}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    nt, r, smem = launch_shape(CAP, 10)
+    nt, r, smem = launch_shape(CAP, 10, mp.end - mp.begin)
     peak_meas = fp32_peak_gflops() / 1e3
     peak = max(peak_meas, FP32_SPEC_TFLOPS)
     flops_per_launch = 12.0 * inter_all / max(world, 1)

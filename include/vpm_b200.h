@@ -178,9 +178,10 @@ double vpm_fp32_peak_probe(int iters, int mode);
  * each, row-major, the attached block with row stride nb).  out: 3 (nb+2)^2. */
 int vpm_boundary_inverse(const int64_t *iparams, const double *fparams, double *out);
 
-/* Launch configuration chosen for a particle cap: threads per rollout CTA,
- * targets per thread, dynamic shared memory bytes. */
-int vpm_launch_shape(int cap, int nb, int *threads, int *targets, int *smem_bytes);
+/* Launch configuration chosen for a particle cap and a batch of rows on the
+ * current device: threads per rollout CTA, targets per thread, dynamic shared
+ * memory bytes. */
+int vpm_launch_shape(int cap, int nb, int rows, int *threads, int *targets, int *smem_bytes);
 
 #ifdef __cplusplus
 }

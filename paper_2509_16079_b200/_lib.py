@@ -119,7 +119,7 @@ def lib():
                                                  C.c_double, C.c_double, _D, _D]),
             "vpm_plan_timing": (C.c_int, [vp, C.c_int, _D, _I64]),
             "vpm_fp32_peak_probe": (C.c_double, [C.c_int, C.c_int]),
-            "vpm_launch_shape": (C.c_int, [C.c_int, C.c_int, _I32, _I32, _I32]),
+            "vpm_launch_shape": (C.c_int, [C.c_int, C.c_int, C.c_int, _I32, _I32, _I32]),
             "vpm_boundary_inverse": (C.c_int, [_I64, _D, _D]),
         }
         for name, (res, args) in sig.items():

@@ -151,39 +151,63 @@ struct Shape {
   int nt, r;
 };
 
-// Smallest tile (threads x targets/thread) covering the cap; deeper register
-// tiles once there are enough particles to keep every thread busy.
-Shape pick_shape(int cap) {
-  static const Shape table[] = {{64, 1}, {64, 2}, {128, 2}, {128, 4}, {256, 4}, {256, 8}, {512, 8}};
-  for (const Shape &s : table)
-    if (s.nt * s.r >= cap) return s;
-  return table[6];
+int device_sms() {
+  static thread_local int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
 }
 
-template <int NT, int R>
-cudaError_t launch_t(const Args &a, int grid, size_t smem, cudaStream_t st) {
-  auto k = vpm::rollout_kernel<NT, R>;
+// Launch shape = (threads per rollout CTA, targets per thread R).  The register
+// tile NT x R covers cap + 4 (the largest wake a snapshot may hold), so every
+// particle is a register target.  NT is the smallest of 64..512 that still puts
+// >= 24 warps on every SM given how many rollouts each SM receives -- 4097
+// rollouts on one GPU take deep tiles (128 x 5), 512 per GPU at 8 GPUs take wider
+// CTAs (256 x 3) -- and R <= 8.  Results do not depend on the shape (canonical
+// reduction orders, see vpm_rollout.cuh).  64 registers/thread.
+Shape pick_shape(int cap, int rows) {
+  const double per_sm = rows > 0 ? (double)rows / device_sms() : 1.0;
+  const int need = cap + 4;
+  Shape best{512, (need + 511) / 512};
+  for (int nt = 64; nt <= 512; nt *= 2) {
+    const int r = (need + nt - 1) / nt;
+    if (r > 8) continue;
+    const double ctas = per_sm < 1024.0 / nt ? per_sm : 1024.0 / nt;
+    if (ctas * nt >= 768.0) return Shape{nt, r};
+    best = Shape{nt, r};
+  }
+  return best;
+}
+
+template <int R>
+cudaError_t launch_t(const Args &a, int grid, int nt, size_t smem, cudaStream_t st) {
+  auto k = vpm::rollout_kernel<R>;
   static thread_local size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  k<<<grid, NT, smem, st>>>(a);
+  k<<<grid, nt, smem, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rollouts(const Args &a, int grid, cudaStream_t st) {
-  const Shape sh = pick_shape(a.P.cap);
+  const Shape sh = pick_shape(a.P.cap, grid);
   const size_t smem = vpm::make_layout(a.P.cap, a.P.nb, sh.nt).total;
-  switch (sh.nt * 16 + sh.r) {
-    case 64 * 16 + 1: return launch_t<64, 1>(a, grid, smem, st);
-    case 64 * 16 + 2: return launch_t<64, 2>(a, grid, smem, st);
-    case 128 * 16 + 2: return launch_t<128, 2>(a, grid, smem, st);
-    case 128 * 16 + 4: return launch_t<128, 4>(a, grid, smem, st);
-    case 256 * 16 + 4: return launch_t<256, 4>(a, grid, smem, st);
-    case 256 * 16 + 8: return launch_t<256, 8>(a, grid, smem, st);
-    default: return launch_t<512, 8>(a, grid, smem, st);
+  switch (sh.r) {
+    case 1: return launch_t<1>(a, grid, sh.nt, smem, st);
+    case 2: return launch_t<2>(a, grid, sh.nt, smem, st);
+    case 3: return launch_t<3>(a, grid, sh.nt, smem, st);
+    case 4: return launch_t<4>(a, grid, sh.nt, smem, st);
+    case 5: return launch_t<5>(a, grid, sh.nt, smem, st);
+    case 6: return launch_t<6>(a, grid, sh.nt, smem, st);
+    case 7: return launch_t<7>(a, grid, sh.nt, smem, st);
+    default: return launch_t<8>(a, grid, sh.nt, smem, st);
   }
 }
 
@@ -218,6 +242,11 @@ struct vpm_plan {
   std::vector<cudaEvent_t> ev;  // start/stop pairs
   size_t ev_used = 0;
   std::mutex mu;
+  // host-buffer optimise path: own stream and grow-only scratch
+  std::mutex host_mu;
+  cudaStream_t hstream = nullptr;
+  void *hscratch = nullptr;
+  size_t hscratch_len = 0;
 };
 
 static Args base_args(const vpm_plan *p) {
@@ -267,8 +296,8 @@ extern "C" {
 
 const char *vpm_last_error(void) { return g_err.c_str(); }
 
-int vpm_launch_shape(int cap, int nb, int *threads, int *targets, int *smem_bytes) {
-  const Shape s = pick_shape(cap);
+int vpm_launch_shape(int cap, int nb, int rows, int *threads, int *targets, int *smem_bytes) {
+  const Shape s = pick_shape(cap, rows);
   if (threads) *threads = s.nt;
   if (targets) *targets = s.r;
   if (smem_bytes) *smem_bytes = vpm::make_layout(cap, nb, s.nt).total;
@@ -319,6 +348,8 @@ void vpm_plan_destroy(vpm_plan *p) {
   cudaFree(p->d_pgam);
   cudaFree(p->d_ema);
   cudaFree(p->d_wbuf);
+  cudaFree(p->hscratch);
+  if (p->hstream) cudaStreamDestroy(p->hstream);
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
   delete p;
 }
@@ -430,21 +461,39 @@ int vpm_mppi_optimize_host(vpm_plan *p, const double *x0, double *u_star, const 
                            int iters, int K, int T, double sigma, double temperature,
                            const double *q, const double *x_perch) {
   if (!p) return fail_cfg("null plan");
+  if (iters < 0 || K < 0 || T < 0) return fail_cfg("negative iterations / batch / horizon");
   CK(cudaSetDevice(p->device));
-  cudaStream_t st;
-  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  std::lock_guard<std::mutex> hl(p->host_mu);
+  if (!p->hstream) CK(cudaStreamCreateWithFlags(&p->hstream, cudaStreamNonBlocking));
+  cudaStream_t st = p->hstream;
   const int B = K + 1;
-  double *d_x0, *d_u, *d_noise, *d_q, *d_xp, *d_cost, *d_part;
-  int32_t *d_flag;
   const size_t nn = (size_t)iters * K * T;
-  CK(cudaMallocAsync(&d_x0, 7 * sizeof(double), st));
-  CK(cudaMallocAsync(&d_u, (T > 0 ? T : 1) * sizeof(double), st));
-  CK(cudaMallocAsync(&d_noise, (nn > 0 ? nn : 1) * sizeof(double), st));
-  CK(cudaMallocAsync(&d_q, 7 * sizeof(double), st));
-  CK(cudaMallocAsync(&d_xp, 7 * sizeof(double), st));
-  CK(cudaMallocAsync(&d_cost, B * sizeof(double), st));
-  CK(cudaMallocAsync(&d_part, (T + 2) * sizeof(double), st));
-  CK(cudaMallocAsync(&d_flag, iters * sizeof(int32_t) + 4, st));
+  // persistent, grow-only device scratch (no per-call allocation)
+  const size_t need = 256 * 8 + sizeof(double) * (7 + (size_t)(T + 1) + nn + 14 + (size_t)B + (T + 2)) +
+                      sizeof(int32_t) * (iters + 1);
+  if (p->hscratch_len < need) {
+    cudaFree(p->hscratch);
+    p->hscratch = nullptr;
+    p->hscratch_len = 0;
+    CK(cudaMalloc(&p->hscratch, need));
+    p->hscratch_len = need;
+  }
+  char *base = (char *)p->hscratch;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    off = (off + 255) & ~(size_t)255;
+    void *r = base + off;
+    off += bytes;
+    return r;
+  };
+  double *d_x0 = (double *)take(7 * sizeof(double));
+  double *d_u = (double *)take((T + 1) * sizeof(double));
+  double *d_noise = (double *)take((nn + 1) * sizeof(double));
+  double *d_q = (double *)take(7 * sizeof(double));
+  double *d_xp = (double *)take(7 * sizeof(double));
+  double *d_cost = (double *)take(B * sizeof(double));
+  double *d_part = (double *)take((T + 2) * sizeof(double));
+  int32_t *d_flag = (int32_t *)take((iters + 1) * sizeof(int32_t));
   CK(cudaMemcpyAsync(d_x0, x0, 7 * sizeof(double), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_u, u_star, T * sizeof(double), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_noise, noise, nn * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -460,16 +509,7 @@ int vpm_mppi_optimize_host(vpm_plan *p, const double *x0, double *u_star, const 
     CK(cudaMemcpyAsync(u_star, d_u, T * sizeof(double), cudaMemcpyDeviceToHost, st));
     if (iters > 0) CK(cudaMemcpyAsync(flags.data(), d_flag, iters * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   }
-  cudaFreeAsync(d_x0, st);
-  cudaFreeAsync(d_u, st);
-  cudaFreeAsync(d_noise, st);
-  cudaFreeAsync(d_q, st);
-  cudaFreeAsync(d_xp, st);
-  cudaFreeAsync(d_cost, st);
-  cudaFreeAsync(d_part, st);
-  cudaFreeAsync(d_flag, st);
   CK(cudaStreamSynchronize(st));
-  CK(cudaStreamDestroy(st));
   if (rc) return rc;
   for (int it = 0; it < iters; ++it)
     if (flags[it]) {

@@ -1,11 +1,11 @@
 // vpm_rollout.cuh -- sm_100a kernels of the VPM-MPPI hot path.
 //
 // One CTA owns one rollout for all H steps.  The wake (<= cap+8 particles) lives
-// in shared memory as float4 {x, z, Gamma/(2 pi), age}; the rigid-body state, the
-// bound-vortex row, the unsteady-load filter and every discrete decision live in
-// a small FP64 control block in shared memory.  The O(N^2) regularised
-// Biot-Savart sweeps run on the FP32 pipe (FFMA + MUFU.RSQ), everything O(1) /
-// O(nb) runs in FP64 on warp 0.
+// in shared memory as float4 {x, z, Gamma/(2 pi), age}, double-buffered; the
+// rigid-body state, the bound-vortex row, the unsteady-load filter and every
+// discrete decision live in an FP64 control block in shared memory.  The O(N^2)
+// regularised Biot-Savart sweeps run on the FP32 pipe (packed FFMA2/FADD2/FMUL2 +
+// MUFU.RSQ); everything O(1) / O(nb) runs in FP64 on warp 0.
 //
 // Reference semantics (paths relative to /root/reference/pkg/src/perchsim/):
 //   step_core         _accel/_core.pyx:175-462  (== vpm.py:635-669 + glider.py:104-122)
@@ -26,9 +26,9 @@
 //       (_core.pyx:483-484), then the chord frame / collocation geometry and the
 //       stall + reversed-flow gates of step t (_core.pyx:228-256).
 //   A   all threads (overlapping D): Euler advection, dissipation, ageing of
-//       their own particles (_core.pyx:222-226), written straight into their
-//       compacted slot (this retires the ordered removals of step t-1); Kelvin
-//       partial sums; per-warp merge candidates.
+//       their own particles (_core.pyx:222-226), read from the raw buffer and
+//       written compacted into the other buffer (this retires the ordered
+//       removals of step t-1); Kelvin block sums; per-warp merge candidates.
 //   B2
 //   S2  all threads: wake velocity at the nb collocation rows (_core.pyx:273-296).
 //   B3
@@ -41,6 +41,14 @@
 //
 // The loads of step t are computed lazily at the top of iteration t+1 because
 // they need exactly the sources of the next convection sweep.
+//
+// Determinism: every floating-point reduction has a canonical order that does not
+// depend on the CTA shape, the batch size or the row range -- per-target sums run
+// over sources in index order (packed and scalar paths are bitwise identical),
+// cross-thread sums are taken over fixed 32-source blocks with a fixed butterfly
+// and then accumulated block by block.  A rollout therefore produces the same
+// bits whatever launch it is part of (the reference's "batch == sequential",
+// _core.pyx:671-676), and every rank count of the sharded planner agrees bitwise.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -49,13 +57,13 @@
 
 namespace vpm {
 
-constexpr int NB_MAX = 64;  // reference MAXNB (_core.pyx:23)
-constexpr int NW_MAX = 16;  // up to 512 threads per rollout
-constexpr int MC = 8;       // merge candidates kept per warp
-constexpr int XMAX = 8;     // overflow wake targets handled source-split
-constexpr int CH = 4;       // source-split targets per chunk
+constexpr int NB_MAX = 64;     // reference MAXNB (_core.pyx:23)
+constexpr int NT_MAX = 512;    // threads per rollout CTA
+constexpr int NW_MAX = NT_MAX / 32;
+constexpr int MC = 8;          // merge candidates kept per warp
+constexpr int CH = 4;          // source-split targets per chunk
 constexpr int HOLES_MAX = 16;
-constexpr int WAKE_PAD = 8;  // wake slots beyond cap (reference buffers hold cap+4)
+constexpr int WAKE_PAD = 8;    // wake slots beyond cap (reference buffers hold cap+4)
 constexpr double TWO_PI = 6.283185307179586476925286766559;
 constexpr double INV_TWO_PI = 0.15915494309189533576888376337251;
 constexpr double PI = 3.14159265358979323846264338327950288;
@@ -115,17 +123,17 @@ struct Ctl {
   int pending;  // loads + integration of the last solved step not yet applied
   int n_raw, n_live, ring_a, ring_b, n_holes;
   int holes[HOLES_MAX];
-  int np_split, nx_split;  // split targets of the next S1: panels, overflow particles
-  int mcnt;                // merge candidates each warp keeps this step
+  int mcnt;     // merge candidates each warp keeps this step
   int fail, status, rc;
+  int cur;      // which of the two wake buffers holds the current (raw) wake
   long long inter;
   unsigned long long shed_mask;
 };
 
 // ---- shared-memory layout (host computes the same size) ----------------------
 struct Layout {
-  int capbuf, nb, S, RS, nw;
-  int off_psrc, off_st, off_ctl, off_d, off_cand, total;
+  int capbuf, nb, S, RS, nw, nblk;
+  int off_psrc, off_st, off_ctl, off_d, off_red, off_cand, total;
 };
 
 __host__ __device__ inline int align16(int v) { return (v + 15) & ~15; }
@@ -135,19 +143,23 @@ __host__ __device__ inline Layout make_layout(int cap, int nb, int nt) {
   L.capbuf = cap + WAKE_PAD;
   L.nb = nb;
   L.S = nb + 2;
-  L.RS = 2 * (nb + XMAX);
+  L.RS = 2 * nb;                      // floats per source block in the split reductions
   L.nw = nt / 32;
-  int off = L.capbuf * 16;
+  L.nblk = (L.capbuf + 31) / 32;      // 32-source blocks
+  int off = 2 * L.capbuf * 16;        // double-buffered wake
   L.off_psrc = off;
   off += nb * 16;
   L.off_st = off;
-  off += (nb + XMAX) * 8;
+  off += nb * 8;
   off = align16(off);
   L.off_ctl = off;
   off += align16((int)sizeof(Ctl));
   L.off_d = off;
-  // cx cz bx bz gam pgp pxp pzp ema bvec (10 S) + pf (3 S) + kel (nw) + red (nw RS)
-  off += (13 * L.S + L.nw + L.nw * L.RS) * 8;
+  // cx cz bx bz gam pgp pxp pzp ema bvec (10 S) + pf (3 S) + Kelvin block sums (nblk)
+  off += (13 * L.S + L.nblk) * 8;
+  off = align16(off);
+  L.off_red = off;
+  off += L.nblk * L.RS * 4;
   off = align16(off);
   L.off_cand = off;
   off += L.nw * MC * 4;
@@ -162,48 +174,84 @@ __device__ __forceinline__ float rsqrt_mufu(float v) {
   return r;
 }
 
-// u += g' [dz, -dx] / sqrt(r^4 + rc^4), g' = Gamma / 2pi   (_core.pyx:89-97)
-__device__ __forceinline__ void bs_accum(float sx, float sz, float sg, float tx, float tz,
-                                         float rc4, float &ux, float &uz) {
-  const float dx = tx - sx;
-  const float dz = tz - sz;
+// One regularised Biot-Savart interaction (_core.pyx:89-97) in the form every
+// path shares bitwise: with d' = s - t and c = g' / sqrt(r^4 + rc^4),
+//   ax += c d'_z   (u_x = -ax)      az += c d'_x   (u_z = +az)
+__device__ __forceinline__ void bs_chain(float sx, float sz, float sg, float ntx, float ntz,
+                                         float rc4, float &ax, float &az) {
+  const float dx = sx + ntx;
+  const float dz = sz + ntz;
   const float r2 = fmaf(dx, dx, dz * dz);
   const float c = sg * rsqrt_mufu(fmaf(r2, r2, rc4));
-  ux = fmaf(c, dz, ux);
-  uz = fmaf(-c, dx, uz);
+  ax = fmaf(c, dz, ax);
+  az = fmaf(c, dx, az);
 }
 
-// Register-tiled sweep: K targets per thread against n sources in shared memory.
+// Register-tiled sweep: K targets per thread against n sources in shared memory,
+// accumulated into (ax, az).  Pairs of targets run on the sm_100 f32x2 path
+// (FADD2 / FMUL2 / FFMA2 take one issue slot for two lanes' worth of FP32 work, so
+// the FMA pipe and the MUFU pipe -- 8 FP32 ops and 1 RSQ per interaction -- can
+// both run near their rates); an odd target uses the scalar twin of the same math.
 template <int K>
 __device__ __forceinline__ void sweep_tile(const float4 *__restrict__ src, int n,
-                                           const float *tx, const float *tz, float *ux,
-                                           float *uz, float rc4) {
-#pragma unroll 4
+                                           const float *ntx, const float *ntz, float *ax,
+                                           float *az, float rc4) {
+  constexpr int KP = K / 2;
+  float2 px[KP > 0 ? KP : 1], pz[KP > 0 ? KP : 1], qx[KP > 0 ? KP : 1], qz[KP > 0 ? KP : 1];
+#pragma unroll
+  for (int p = 0; p < KP; ++p) {
+    px[p] = make_float2(ntx[2 * p], ntx[2 * p + 1]);
+    pz[p] = make_float2(ntz[2 * p], ntz[2 * p + 1]);
+    qx[p] = make_float2(ax[2 * p], ax[2 * p + 1]);
+    qz[p] = make_float2(az[2 * p], az[2 * p + 1]);
+  }
+  const float2 rc = make_float2(rc4, rc4);
+  float ox = (K & 1) ? ax[K - 1] : 0.f, oz = (K & 1) ? az[K - 1] : 0.f;
+#pragma unroll 2
   for (int j = 0; j < n; ++j) {
     const float4 s = src[j];
+    const float2 sx = make_float2(s.x, s.x), sz = make_float2(s.y, s.y), sg = make_float2(s.z, s.z);
 #pragma unroll
-    for (int k = 0; k < K; ++k) bs_accum(s.x, s.y, s.z, tx[k], tz[k], rc4, ux[k], uz[k]);
+    for (int p = 0; p < KP; ++p) {
+      const float2 dx = __fadd2_rn(sx, px[p]);
+      const float2 dz = __fadd2_rn(sz, pz[p]);
+      const float2 r2 = __ffma2_rn(dx, dx, __fmul2_rn(dz, dz));
+      const float2 q = __ffma2_rn(r2, r2, rc);
+      const float2 rs = make_float2(rsqrt_mufu(q.x), rsqrt_mufu(q.y));
+      const float2 c = __fmul2_rn(sg, rs);
+      qx[p] = __ffma2_rn(c, dz, qx[p]);
+      qz[p] = __ffma2_rn(c, dx, qz[p]);
+    }
+    if constexpr (K & 1) bs_chain(s.x, s.y, s.z, ntx[K - 1], ntz[K - 1], rc4, ox, oz);
+  }
+#pragma unroll
+  for (int p = 0; p < KP; ++p) {
+    ax[2 * p] = qx[p].x;
+    ax[2 * p + 1] = qx[p].y;
+    az[2 * p] = qz[p].x;
+    az[2 * p + 1] = qz[p].y;
+  }
+  if constexpr (K & 1) {
+    ax[K - 1] = ox;
+    az[K - 1] = oz;
   }
 }
 
+// kw = number of target slots with at least one live lane in this warp (uniform)
 template <int R>
-__device__ __forceinline__ void sweep_dispatch(int kw, const float4 *src, int n, const float *tx,
-                                               const float *tz, float *ux, float *uz, float rc4) {
-  // kw = number of target slots live in this warp (warp-uniform)
-  if constexpr (R >= 8) {
-    if (kw == 8) { sweep_tile<8>(src, n, tx, tz, ux, uz, rc4); return; }
-    if (kw == 7) { sweep_tile<7>(src, n, tx, tz, ux, uz, rc4); return; }
-    if (kw == 6) { sweep_tile<6>(src, n, tx, tz, ux, uz, rc4); return; }
-    if (kw == 5) { sweep_tile<5>(src, n, tx, tz, ux, uz, rc4); return; }
+__device__ __forceinline__ void sweep_dispatch(int kw, const float4 *src, int n, const float *ntx,
+                                               const float *ntz, float *ax, float *az, float rc4) {
+  switch (kw) {
+    case 8: if constexpr (R >= 8) sweep_tile<8>(src, n, ntx, ntz, ax, az, rc4); break;
+    case 7: if constexpr (R >= 7) sweep_tile<7>(src, n, ntx, ntz, ax, az, rc4); break;
+    case 6: if constexpr (R >= 6) sweep_tile<6>(src, n, ntx, ntz, ax, az, rc4); break;
+    case 5: if constexpr (R >= 5) sweep_tile<5>(src, n, ntx, ntz, ax, az, rc4); break;
+    case 4: if constexpr (R >= 4) sweep_tile<4>(src, n, ntx, ntz, ax, az, rc4); break;
+    case 3: if constexpr (R >= 3) sweep_tile<3>(src, n, ntx, ntz, ax, az, rc4); break;
+    case 2: if constexpr (R >= 2) sweep_tile<2>(src, n, ntx, ntz, ax, az, rc4); break;
+    case 1: sweep_tile<1>(src, n, ntx, ntz, ax, az, rc4); break;
+    default: break;
   }
-  if constexpr (R >= 4) {
-    if (kw == 4) { sweep_tile<4>(src, n, tx, tz, ux, uz, rc4); return; }
-    if (kw == 3) { sweep_tile<3>(src, n, tx, tz, ux, uz, rc4); return; }
-  }
-  if constexpr (R >= 2) {
-    if (kw == 2) { sweep_tile<2>(src, n, tx, tz, ux, uz, rc4); return; }
-  }
-  if (kw >= 1) sweep_tile<1>(src, n, tx, tz, ux, uz, rc4);
 }
 
 // Deterministic butterfly-transpose reduction of 8 floats across a warp:
@@ -246,33 +294,49 @@ __device__ __forceinline__ int raw_index(int c, const int *holes, int nh) {
   return r;
 }
 
-// Source-split sweep: targets tgt[0..nt) (float2), every thread takes sources
-// j = tid, tid+NT, ... of src[0..n); per-warp sums land in red[warp*RS + 2k(+1)].
-template <int NT>
+// Source-split sweep for a handful of targets tgt[0..nt): warp w takes the
+// 32-source blocks b = w, w+NW, ...; lane l the source 32b + l.  Each block's
+// contribution is reduced with the fixed butterfly and stored per block in
+// red[b * RS + 2k (+1)] = (sum c d'_z, sum c d'_x); consumers add blocks in order.
 __device__ __forceinline__ void split_sweep(const float4 *__restrict__ src, int n,
-                                            const float2 *tgt, int nt, float rc4, double *red,
-                                            int RS, int tid) {
-  const int lane = tid & 31, warp = tid >> 5;
+                                            const float2 *tgt, int nt, float rc4, float *red,
+                                            int RS, int warp, int lane, int nw) {
+  const int nblk = (n + 31) >> 5;
   for (int c0 = 0; c0 < nt; c0 += CH) {
-    float tx[CH], tz[CH];
+    float ntx[CH], ntz[CH];
 #pragma unroll
     for (int k = 0; k < CH; ++k) {
       const int i = c0 + k < nt ? c0 + k : nt - 1;
-      tx[k] = tgt[i].x;
-      tz[k] = tgt[i].y;
+      ntx[k] = -tgt[i].x;
+      ntz[k] = -tgt[i].y;
     }
-    float acc[2 * CH];
+    for (int b = warp; b < nblk; b += nw) {
+      const int j = 32 * b + lane;
+      float acc[2 * CH];
 #pragma unroll
-    for (int k = 0; k < 2 * CH; ++k) acc[k] = 0.f;
-    for (int j = tid; j < n; j += NT) {
-      const float4 s = src[j];
+      for (int k = 0; k < 2 * CH; ++k) acc[k] = 0.f;
+      if (j < n) {
+        const float4 s = src[j];
 #pragma unroll
-      for (int k = 0; k < CH; ++k) bs_accum(s.x, s.y, s.z, tx[k], tz[k], rc4, acc[2 * k], acc[2 * k + 1]);
+        for (int k = 0; k < CH; ++k) bs_chain(s.x, s.y, s.z, ntx[k], ntz[k], rc4, acc[2 * k], acc[2 * k + 1]);
+      }
+      const float r = warp_reduce8(acc, lane);
+      const int vi = lane >> 2;  // value index: target c0 + vi/2, component vi&1
+      if ((lane & 3) == 0 && c0 + (vi >> 1) < nt) red[b * RS + 2 * c0 + vi] = r;
     }
-    const float r = warp_reduce8(acc, lane);
-    const int vi = lane >> 2;  // value index: target c0 + vi/2, component vi&1
-    if ((lane & 3) == 0 && c0 + (vi >> 1) < nt) red[warp * RS + 2 * c0 + vi] = (double)r;
   }
+}
+
+// wake velocity at split target k from the per-block partials (block order)
+__device__ __forceinline__ void split_result(const float *red, int RS, int nblk, int k, double &ux,
+                                             double &uz) {
+  double sx = 0.0, sz = 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    sx += (double)red[b * RS + 2 * k];
+    sz += (double)red[b * RS + 2 * k + 1];
+  }
+  ux = -sx;
+  uz = sz;
 }
 
 __device__ __forceinline__ double clampd(double v, double lo, double hi) {
@@ -293,14 +357,16 @@ __device__ __forceinline__ double control_at(const Args &a, int row, int t) {
 }
 
 // ---- the rollout kernel -------------------------------------------------------------
-template <int NT, int R>
-__global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
-  constexpr int NW = NT / 32;
+// R = register-tile targets per thread; blockDim.x * R >= cap + 4 (host guarantees),
+// so every live particle is a register target.
+template <int R>
+__global__ void __launch_bounds__(NT_MAX, 2) rollout_kernel(const Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Phys &P = a.P;
   const int nb = P.nb;
+  const int NT = blockDim.x, NW = NT >> 5;
   const Layout L = make_layout(P.cap, nb, NT);
-  float4 *wk = reinterpret_cast<float4 *>(smem);
+  float4 *wbuf = reinterpret_cast<float4 *>(smem);  // two wake buffers of capbuf
   float4 *psrc = reinterpret_cast<float4 *>(smem + L.off_psrc);
   float2 *st = reinterpret_cast<float2 *>(smem + L.off_st);
   Ctl *ctl = reinterpret_cast<Ctl *>(smem + L.off_ctl);
@@ -308,7 +374,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
   const int S = L.S, RS = L.RS;
   double *cx = dsh, *cz = dsh + S, *bx = dsh + 2 * S, *bz = dsh + 3 * S, *gam = dsh + 4 * S;
   double *pgp = dsh + 5 * S, *pxp = dsh + 6 * S, *pzp = dsh + 7 * S, *ema = dsh + 8 * S;
-  double *bvec = dsh + 9 * S, *pf = dsh + 10 * S, *kel = dsh + 13 * S, *red = kel + NW;
+  double *bvec = dsh + 9 * S, *pf = dsh + 10 * S, *kblk = dsh + 13 * S;
+  float *red = reinterpret_cast<float *>(smem + L.off_red);
   unsigned *cand = reinterpret_cast<unsigned *>(smem + L.off_cand);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -316,12 +383,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
   const int T = a.T;
   const float rc4 = P.rc4f;
   const double dt = P.dt;
-  constexpr int TILE = NT * R;
 
   // ---- prologue: fork the snapshot into shared memory (_core.pyx:494-526)
   for (int i = tid; i < a.n_wake; i += NT)
-    wk[i] = make_float4((float)a.wpos[2 * i], (float)a.wpos[2 * i + 1],
-                        (float)(a.wgam[i] * INV_TWO_PI), __int_as_float((int)a.wage[i]));
+    wbuf[i] = make_float4((float)a.wpos[2 * i], (float)a.wpos[2 * i + 1],
+                          (float)(a.wgam[i] * INV_TWO_PI), __int_as_float((int)a.wage[i]));
   for (int j = tid; j < a.n_prev; j += NT)
     psrc[j] = make_float4((float)a.ppos[2 * j], (float)a.ppos[2 * j + 1],
                           (float)(a.pgam[j] * INV_TWO_PI), 0.f);
@@ -338,8 +404,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
       ctl->x[lane] = x0[lane];
       if (a.record && a.trajs) a.trajs[(size_t)row * (T + 1) * 7 + lane] = x0[lane];
     }
-    const int xs = a.n_wake > TILE ? min(XMAX, a.n_wake - TILE) : 0;
-    if (lane < xs) st[lane] = make_float2((float)a.wpos[2 * (TILE + lane)], (float)a.wpos[2 * (TILE + lane) + 1]);
     if (lane == 0) {
       ctl->n_raw = a.n_wake;
       ctl->n_live = a.n_wake;
@@ -350,8 +414,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
       ctl->lev_prev = a.prev_lev;
       ctl->lev_cur = 0.0;
       ctl->pending = 0;
-      ctl->np_split = 0;
-      ctl->nx_split = xs;
       ctl->mcnt = min(MC, max(0, a.n_wake + 3 - P.cap));
       ctl->fail = 0;
       ctl->status = 0;
@@ -361,6 +423,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
       ctl->fwx = ctl->fwz = ctl->mw = 0.0;
       ctl->hp = 0;
       ctl->shed = ctl->rev = 0;
+      ctl->cur = 0;
     }
   }
   __syncthreads();
@@ -369,36 +432,41 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
     const bool conv = t < T;
     const bool pend = ctl->pending;
     const int n_raw = ctl->n_raw, n_live = ctl->n_live, nh = ctl->n_holes;
-    const int np_s = pend ? ctl->np_split : 0;
-    const int nx_s = conv ? ctl->nx_split : 0;
     const int n_prev = ctl->n_prev;
+    const int cur = ctl->cur;
+    const float4 *wsrc = wbuf + cur * L.capbuf;  // raw wake of this iteration (read-only)
+    float4 *wk = wbuf + (cur ^ 1) * L.capbuf;    // compacted, advected wake being built
 
     // ---------------- S1: convection sweep (+ loads sweep of step t-1)
-    float tx[R], tz[R], tg[R], ux[R], uz[R];
-    int tage[R];
-    int kw = 0;
+    float ux[R], uz[R];
     if (conv) {
-      const int nwt = min(n_live, TILE);
+      float ntx[R], ntz[R], bx_[R], bz_[R];
+      int kw = 0;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         const int c = tid + NT * k;
+        ntx[k] = 0.f;
+        ntz[k] = 0.f;
+        if (c < n_live) {
+          const float4 v = wsrc[raw_index(c, ctl->holes, nh)];
+          ntx[k] = -v.x;
+          ntz[k] = -v.y;
+        }
+        if (32 * warp + NT * k < n_live) kw = k + 1;
         ux[k] = 0.f;
         uz[k] = 0.f;
-        if (c < nwt) {
-          const float4 v = wk[raw_index(c, ctl->holes, nh)];
-          tx[k] = v.x; tz[k] = v.y; tg[k] = v.z; tage[k] = __float_as_int(v.w);
-        } else {
-          tx[k] = 0.f; tz[k] = 0.f; tg[k] = 0.f; tage[k] = 0;
-        }
+        bx_[k] = 0.f;
+        bz_[k] = 0.f;
       }
-      const int wbase = warp * 32;
+      sweep_dispatch<R>(kw, wsrc, n_raw, ntx, ntz, ux, uz, rc4);
+      sweep_dispatch<R>(kw, psrc, n_prev, ntx, ntz, bx_, bz_, rc4);
 #pragma unroll
-      for (int k = 0; k < R; ++k)
-        if (wbase + NT * k < nwt) kw = k + 1;
-      sweep_dispatch<R>(kw, wk, n_raw, tx, tz, ux, uz, rc4);
-      sweep_dispatch<R>(kw, psrc, n_prev, tx, tz, ux, uz, rc4);
+      for (int k = 0; k < R; ++k) {
+        ux[k] = -ux[k] - bx_[k];  // u_x = -(wake chain) - (bound-row chain)
+        uz[k] = uz[k] + bz_[k];
+      }
     }
-    if (np_s + nx_s > 0) split_sweep<NT>(wk, n_raw, st, np_s + nx_s, rc4, red, RS, tid);
+    if (pend) split_sweep(wsrc, n_raw, st, nb, rc4, red, RS, warp, lane, NW);
     __syncthreads();  // B1
 
     // ---------------- D: loads + integration of step t-1, geometry of step t
@@ -409,9 +477,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
         const int hp = ctl->hp;
         const double xwx = rx - P.l_w * fx, xwz = rz - P.l_w * fz;
         const double dlev = hp ? (ctl->lev_cur - ctl->lev_prev) / dt : 0.0;
+        const int nblk1 = (n_raw + 31) >> 5;
         for (int p = lane; p < nb; p += 32) {
-          double uxp = 0.0, uzp = 0.0;
-          for (int w = 0; w < NW; ++w) { uxp += red[w * RS + 2 * p]; uzp += red[w * RS + 2 * p + 1]; }
+          double uxp, uzp;
+          split_result(red, RS, nblk1, p, uxp, uzp);
           double cum = 0.0, cum_prev = 0.0;
           for (int i = 0; i <= p; ++i) { cum += gam[i]; cum_prev += pgp[i]; }
           const double rate = hp ? (cum - cum_prev) / dt + dlev : 0.0;
@@ -511,65 +580,44 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
     }
 
     // ---------------- A: advect / dissipate / age into compacted slots
+    // (reads the raw buffer, writes the other one: no read/write race, and on a
+    //  failure in D the raw buffer still holds the reference's failure-time wake)
     if (conv) {
-      if (a.need_fluid) {
-        __syncthreads();
-        if (ctl->fail) break;
-      }
       const int ra = ctl->ring_a, rb = ctl->ring_b;
-      const int nwt = min(n_live, TILE);
-      double ksum = 0.0;
-      unsigned keys[R + 1];
+      unsigned keys[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         const int c = tid + NT * k;
         keys[k] = 0u;
-        if (c < nwt) {
-          const float nxp = (float)((double)tx[k] + dt * (double)ux[k]);
-          const float nzp = (float)((double)tz[k] + dt * (double)uz[k]);
-          const float ng = (float)((double)tg[k] * P.k_diss);
-          const int na = tage[k] + 1;
-          wk[c] = make_float4(nxp, nzp, ng, __int_as_float(na));
-          ksum += (double)ng;
-          if (c != ra && c != rb) keys[k] = ((unsigned)(na + 1) << 12) | (unsigned)(4095 - c);
-        }
-      }
-      keys[R] = 0u;
-      if (warp == 0 && nx_s > 0) {
-        // overflow particles beyond the register tile (only when n_live > NT*R)
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        int c = TILE + lane;
-        float vx = 0.f, vz = 0.f;
-        if (lane < nx_s) {
-          v = wk[raw_index(c, ctl->holes, nh)];
-          double sx = 0.0, sz = 0.0;
-          for (int w = 0; w < NW; ++w) { sx += red[w * RS + 2 * (np_s + lane)]; sz += red[w * RS + 2 * (np_s + lane) + 1]; }
-          vx = (float)sx; vz = (float)sz;
-          for (int j = 0; j < n_prev; ++j) { const float4 p = psrc[j]; bs_accum(p.x, p.y, p.z, v.x, v.y, rc4, vx, vz); }
-        }
-        __syncwarp();
-        if (lane < nx_s) {
+        double g = 0.0;
+        if (c < n_live) {
+          const float4 v = wsrc[raw_index(c, ctl->holes, nh)];
+          const float nxp = (float)((double)v.x + dt * (double)ux[k]);
+          const float nzp = (float)((double)v.y + dt * (double)uz[k]);
           const float ng = (float)((double)v.z * P.k_diss);
           const int na = __float_as_int(v.w) + 1;
-          wk[c] = make_float4((float)((double)v.x + dt * (double)vx), (float)((double)v.y + dt * (double)vz), ng, __int_as_float(na));
-          ksum += (double)ng;
-          if (c != ra && c != rb) keys[R] = ((unsigned)(na + 1) << 12) | (unsigned)(4095 - c);
+          wk[c] = make_float4(nxp, nzp, ng, __int_as_float(na));
+          g = (double)ng;
+          if (c != ra && c != rb) keys[k] = ((unsigned)(na + 1) << 12) | (unsigned)(4095 - c);
+        }
+        // Kelvin sum over the canonical 32-particle block c / 32 = warp + NW k
+        if (32 * warp + NT * k < n_live) {
+          g = warp_sum_d(g);
+          if (lane == 0) kblk[warp + NW * k] = g;
         }
       }
-      ksum = warp_sum_d(ksum);
-      if (lane == 0) kel[warp] = ksum;
       const int mc = ctl->mcnt;
       for (int r = 0; r < mc; ++r) {
         unsigned best = 0u;
         int bi = -1;
 #pragma unroll
-        for (int k = 0; k <= R; ++k)
+        for (int k = 0; k < R; ++k)
           if (keys[k] > best) { best = keys[k]; bi = k; }
         const unsigned w = __reduce_max_sync(0xffffffffu, best);
         if (lane == 0) cand[warp * MC + r] = w;
         if (w != 0u && best == w) {
 #pragma unroll
-          for (int k = 0; k <= R; ++k)
+          for (int k = 0; k < R; ++k)
             if (k == bi) keys[k] = 0u;
         }
       }
@@ -581,13 +629,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
     {
       const int shed_rev = ctl->shed && ctl->rev;
       // rows: skip the upstream edge point (_core.pyx:274-275)
-      float2 *rows = st;  // reuse the split-target buffer (S1 consumers are done)
       for (int i = tid; i < nb; i += NT) {
         const int ri = shed_rev ? i : i + 1;
-        rows[i] = make_float2((float)cx[ri], (float)cz[ri]);
+        st[i] = make_float2((float)cx[ri], (float)cz[ri]);
       }
       __syncthreads();
-      split_sweep<NT>(wk, ctl->n_live, rows, nb, rc4, red, RS, tid);
+      split_sweep(wk, n_live, st, nb, rc4, red, RS, warp, lane, NW);
     }
     __syncthreads();  // B3
 
@@ -595,12 +642,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
     if (warp == 0) {
       const int shed = ctl->shed, rev = ctl->rev;
       const int ns = shed ? nb + 2 : nb, r0 = shed ? 1 : 0;
-      const int nl = ctl->n_live;
+      const int nl = n_live;
+      const int nblk2 = (nl + 31) >> 5;
       const double rx = ctl->x[0], rz = ctl->x[1], vx = ctl->x[4], vz = ctl->x[5], om = ctl->x[6];
       const double nx = ctl->nx, nz = ctl->nz;
       for (int i = lane; i < nb; i += 32) {
-        double uxw = 0.0, uzw = 0.0;
-        for (int w = 0; w < NW; ++w) { uxw += red[w * RS + 2 * i]; uzw += red[w * RS + 2 * i + 1]; }
+        double uxw, uzw;
+        split_result(red, RS, nblk2, i, uxw, uzw);
         const int ri = (shed && rev) ? i : i + 1;
         const double px = cx[ri], pz = cz[ri];
         const double svx = vx + om * (-(pz - rz)), svz = vz + om * (px - rx);
@@ -610,7 +658,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
         const int epan = rev ? nb - 1 : 0;
         bvec[0] = P.lev_gain * (ctl->n_prev > 0 ? pgp[epan] : 0.0);
         double tot = 0.0;
-        for (int w = 0; w < NW; ++w) tot += kel[w];
+        for (int b = 0; b < nblk2; ++b) tot += kblk[b];
         bvec[nb + 1] = -(tot * TWO_PI);
       }
       __syncwarp();
@@ -628,7 +676,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
       if (!ok) {
         if (lane == 0) {
           ctl->fail = 1; ctl->status = t + 1; ctl->rc = 2;
-          ctl->n_raw = nl; ctl->n_holes = 0;
+          ctl->n_raw = nl; ctl->n_holes = 0; ctl->cur = cur ^ 1;
         }
       } else {
         const double levg = shed ? gam[nb] : 0.0;
@@ -674,7 +722,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
           }
           if (nsel >= 2) {
             const int merges = min(m, nsel - 1);
-            int idx0 = 4095 - (int)(sel[0] & 4095u);
+            const int idx0 = 4095 - (int)(sel[0] & 4095u);
             float4 blob = wk[idx0];
             int lo = idx0;
             int ids[MC];
@@ -734,23 +782,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
           if (rb >= 0 && hl[h] < rb) --rb2;
         }
         const int n_live_next = n_now - nholes;
-        // previous bound row for the next convection sweep; panels as split targets
+        // previous bound row: sources of the next convection sweep, and the
+        // panels are the split targets of the next loads sweep
         for (int p = lane; p < nb; p += 32) {
           psrc[p] = make_float4((float)bx[p], (float)bz[p], (float)(gam[p] * INV_TWO_PI), 0.f);
           st[p] = make_float2((float)bx[p], (float)bz[p]);
-        }
-        const int xs = n_live_next > TILE ? min(XMAX, n_live_next - TILE) : 0;
-        if (lane < xs) {
-          const int r = raw_index(TILE + lane, hl, nholes);
-          st[nb + lane] = make_float2(wk[r].x, wk[r].y);
         }
         if (lane == 0) {
           ctl->lev_cur = levg;
           ctl->hp = ctl->n_prev > 0;
           ctl->n_prev = nb;
           ctl->pending = 1;
-          ctl->np_split = nb;
-          ctl->nx_split = xs;
           ctl->n_raw = n_now;
           ctl->n_live = n_live_next;
           ctl->n_holes = nholes;
@@ -758,6 +800,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
           ctl->ring_a = ra2;
           ctl->ring_b = rb2;
           ctl->mcnt = min(MC, max(0, n_live_next + 3 - P.cap));
+          ctl->cur = cur ^ 1;
           if (shed && t < 64) ctl->shed_mask |= 1ull << t;
           ctl->inter += (long long)nl * (nl - 1) + (long long)n_prev * nl + (long long)nb * nl +
                         (long long)nb * n_live_next;
@@ -788,9 +831,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) rollout_kernel(const Args a) {
   if (a.need_fluid && row == 0) {
     const int cap4 = P.cap + 4;
     const int nl = ctl->n_live, nh = ctl->n_holes;
+    const float4 *wfin = wbuf + ctl->cur * L.capbuf;
     for (int c = tid; c < cap4; c += NT) {
       if (c < nl) {
-        const float4 v = wk[raw_index(c, ctl->holes, nh)];
+        const float4 v = wfin[raw_index(c, ctl->holes, nh)];
         a.o_wpos[2 * c] = v.x;
         a.o_wpos[2 * c + 1] = v.y;
         a.o_wgam[c] = (double)v.z * TWO_PI;
@@ -916,24 +960,16 @@ template <int MODE>
 __global__ void fp32_probe_kernel(float *out, int iters, float a, float b) {
   float s = 0.f;
   if constexpr (MODE == 1) {
-    unsigned long long v[8], A, Bv;
-    const float2 af = make_float2(a, a), bf = make_float2(b, b);
-    A = *reinterpret_cast<const unsigned long long *>(&af);
-    Bv = *reinterpret_cast<const unsigned long long *>(&bf);
+    float2 v[8];
+    const float2 A = make_float2(a, a), Bv = make_float2(b, b);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float2 t = make_float2(threadIdx.x * 1e-3f + i, 0.5f * i);
-      v[i] = *reinterpret_cast<const unsigned long long *>(&t);
-    }
+    for (int i = 0; i < 8; ++i) v[i] = make_float2(threadIdx.x * 1e-3f + i, 0.5f * i);
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(v[i]) : "l"(A), "l"(Bv));
+      for (int i = 0; i < 8; ++i) v[i] = __ffma2_rn(v[i], A, Bv);
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float2 t = *reinterpret_cast<const float2 *>(&v[i]);
-      s += t.x + t.y;
-    }
+    for (int i = 0; i < 8; ++i) s += v[i].x + v[i].y;
   } else {
     float v[8];
 #pragma unroll

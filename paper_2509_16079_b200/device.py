@@ -142,9 +142,9 @@ def mppi_combine(partials, temperature: float, ustar, flag=None, stream=None):
                                       _p(flag), _stream(stream)), "mppi_combine")
 
 
-def launch_shape(cap: int, nb: int):
+def launch_shape(cap: int, nb: int, rows: int):
     t, r, s = (np.zeros(1, np.int32) for _ in range(3))
-    _lib.lib().vpm_launch_shape(int(cap), int(nb), ptr(t, _I32), ptr(r, _I32), ptr(s, _I32))
+    _lib.lib().vpm_launch_shape(int(cap), int(nb), int(rows), ptr(t, _I32), ptr(r, _I32), ptr(s, _I32))
     return int(t[0]), int(r[0]), int(s[0])
 
 
