@@ -17,10 +17,10 @@ import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "lib", "libvpm_b200.so")
+LIB_PATH = os.environ.get("VPM_LIB") or os.path.join(PKG, "lib", "libvpm_b200.so")
 SOURCES = [os.path.join(PKG, "csrc", "vpm_capi.cu"), os.path.join(PKG, "csrc", "vpm_rollout.cuh"),
            os.path.join(ROOT, "include", "vpm_b200.h")]
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17", "-fmad=false",
               "-shared", "-Xcompiler", "-fPIC"]
 
 VPM_OK, VPM_ERR_CONFIG, VPM_ERR_CUDA, VPM_ERR_ALLFAIL = 0, -1, -2, -3

@@ -148,7 +148,7 @@ int build_inverses(const Phys &P, std::vector<double> &out) {
 }
 
 struct Shape {
-  int nt, r;
+  int nt, r, w0, minb;  // threads, slots per sweeping warp, control-warp slots, reg variant
 };
 
 int device_sms() {
@@ -162,30 +162,41 @@ int device_sms() {
   return sms;
 }
 
-// Launch shape = (threads per rollout CTA, targets per thread R).  The register
-// tile NT x R covers cap + 4 (the largest wake a snapshot may hold), so every
-// particle is a register target.  NT is the smallest of 64..512 that still puts
-// >= 24 warps on every SM given how many rollouts each SM receives -- 4097
-// rollouts on one GPU take deep tiles (128 x 5), 512 per GPU at 8 GPUs take wider
-// CTAs (256 x 3) -- and R <= 8.  Results do not depend on the shape (canonical
-// reduction orders, see vpm_rollout.cuh).  64 registers/thread.
+// Launch shape.  A rollout CTA has NT threads; each holds R register target slots
+// (slot k of warp w = particles 32 (NW k + w) .. +31) covering cap + 4 (the
+// largest wake a snapshot may hold), so every particle is a register target.
+// Warp 0 runs the FP64 loads / dynamics / geometry phase before its slots.  NT is
+// the smallest of 64..512 that still puts >= 24 warps on every SM given how many
+// rollouts each SM receives (4097 rollouts on one GPU -> 128 x 5, 512 per GPU at
+// 8 GPUs -> 256 x 3).  Results do not depend on the shape (canonical reduction
+// orders, see vpm_rollout.cuh).  VPM_SHAPE="nt,r" / VPM_MAXREG override for tuning.
 Shape pick_shape(int cap, int rows) {
-  const double per_sm = rows > 0 ? (double)rows / device_sms() : 1.0;
   const int need = cap + 4;
-  Shape best{512, (need + 511) / 512};
+  if (const char *e = getenv("VPM_SHAPE")) {
+    Shape s{0, 0, 0, 64};
+    if (sscanf(e, "%d,%d", &s.nt, &s.r) == 2 && s.nt >= 64 && s.nt <= vpm::NT_MAX &&
+        s.nt % 32 == 0 && s.r >= 1 && s.r <= 8 && s.nt * s.r >= need) {
+      if (const char *m = getenv("VPM_MAXREG")) s.minb = atoi(m);
+      return s;
+    }
+  }
+  const double per_sm = rows > 0 ? (double)rows / device_sms() : 1.0;
+  Shape best{512, 8, 0, 64};
   for (int nt = 64; nt <= 512; nt *= 2) {
     const int r = (need + nt - 1) / nt;
     if (r > 8) continue;
+    best = Shape{nt, r, 0, 64};
+    if (nt >= need) break;  // more lanes than particles
     const double ctas = per_sm < 1024.0 / nt ? per_sm : 1024.0 / nt;
-    if (ctas * nt >= 768.0) return Shape{nt, r};
-    best = Shape{nt, r};
+    if (ctas * nt >= 768.0) break;
   }
+  if (const char *m = getenv("VPM_MAXREG")) best.minb = atoi(m);
   return best;
 }
 
-template <int R>
+template <int R, int MINB>
 cudaError_t launch_t(const Args &a, int grid, int nt, size_t smem, cudaStream_t st) {
-  auto k = vpm::rollout_kernel<R>;
+  auto k = vpm::rollout_kernel<R, MINB>;
   static thread_local size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -196,18 +207,27 @@ cudaError_t launch_t(const Args &a, int grid, int nt, size_t smem, cudaStream_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_rollouts(const Args &a, int grid, cudaStream_t st) {
+template <int MINB>
+cudaError_t launch_r(const Args &a, int grid, const Shape &sh, size_t smem, cudaStream_t st) {
+  switch (sh.r) {
+    case 1: return launch_t<1, MINB>(a, grid, sh.nt, smem, st);
+    case 2: return launch_t<2, MINB>(a, grid, sh.nt, smem, st);
+    case 3: return launch_t<3, MINB>(a, grid, sh.nt, smem, st);
+    case 4: return launch_t<4, MINB>(a, grid, sh.nt, smem, st);
+    case 5: return launch_t<5, MINB>(a, grid, sh.nt, smem, st);
+    case 6: return launch_t<6, MINB>(a, grid, sh.nt, smem, st);
+    case 7: return launch_t<7, MINB>(a, grid, sh.nt, smem, st);
+    default: return launch_t<8, MINB>(a, grid, sh.nt, smem, st);
+  }
+}
+
+cudaError_t launch_rollouts(Args a, int grid, cudaStream_t st) {
   const Shape sh = pick_shape(a.P.cap, grid);
   const size_t smem = vpm::make_layout(a.P.cap, a.P.nb, sh.nt).total;
-  switch (sh.r) {
-    case 1: return launch_t<1>(a, grid, sh.nt, smem, st);
-    case 2: return launch_t<2>(a, grid, sh.nt, smem, st);
-    case 3: return launch_t<3>(a, grid, sh.nt, smem, st);
-    case 4: return launch_t<4>(a, grid, sh.nt, smem, st);
-    case 5: return launch_t<5>(a, grid, sh.nt, smem, st);
-    case 6: return launch_t<6>(a, grid, sh.nt, smem, st);
-    case 7: return launch_t<7>(a, grid, sh.nt, smem, st);
-    default: return launch_t<8>(a, grid, sh.nt, smem, st);
+  switch (sh.minb) {
+    case 72: return launch_r<72>(a, grid, sh, smem, st);
+    case 80: return launch_r<80>(a, grid, sh, smem, st);
+    default: return launch_r<64>(a, grid, sh, smem, st);
   }
 }
 

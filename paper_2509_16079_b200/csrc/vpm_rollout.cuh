@@ -64,6 +64,10 @@ constexpr int MC = 8;          // merge candidates kept per warp
 constexpr int CH = 4;          // source-split targets per chunk
 constexpr int HOLES_MAX = 16;
 constexpr int WAKE_PAD = 8;    // wake slots beyond cap (reference buffers hold cap+4)
+#ifndef VPM_D_PASS
+#define VPM_D_PASS 1
+#endif
+constexpr int D_PASS = VPM_D_PASS;  // warp 0 runs its control phase after (1) / before (0) its sweep
 constexpr double TWO_PI = 6.283185307179586476925286766559;
 constexpr double INV_TWO_PI = 0.15915494309189533576888376337251;
 constexpr double PI = 3.14159265358979323846264338327950288;
@@ -237,9 +241,13 @@ __device__ __forceinline__ void sweep_tile(const float4 *__restrict__ src, int n
   }
 }
 
-// kw = number of target slots with at least one live lane in this warp (uniform)
+// kw = number of target slots with at least one live lane in this warp (uniform).
+// Not inlined on purpose: the sweep loop then gets the whole register budget for
+// its interleaved interaction chains instead of sharing it with the kernel's
+// outer state (inlined, ptxas serialised the chains through one temporary pair
+// and MUFU latency went exposed); the call costs a few spills per step.
 template <int R>
-__device__ __forceinline__ void sweep_dispatch(int kw, const float4 *src, int n, const float *ntx,
+__device__ __noinline__ void sweep_dispatch(int kw, const float4 *src, int n, const float *ntx,
                                                const float *ntz, float *ax, float *az, float rc4) {
   switch (kw) {
     case 8: if constexpr (R >= 8) sweep_tile<8>(src, n, ntx, ntz, ax, az, rc4); break;
@@ -357,10 +365,11 @@ __device__ __forceinline__ double control_at(const Args &a, int row, int t) {
 }
 
 // ---- the rollout kernel -------------------------------------------------------------
-// R = register-tile targets per thread; blockDim.x * R >= cap + 4 (host guarantees),
-// so every live particle is a register target.
-template <int R>
-__global__ void __launch_bounds__(NT_MAX, 2) rollout_kernel(const Args a) {
+// R = register-tile target slots per thread; blockDim.x * R >= cap + 4 (host
+// guarantees), so every live particle is a register target.  MAXREG = register
+// budget per thread (64: 8 CTAs of 128 threads per SM, 72: 7, 80: 6).
+template <int R, int MAXREG>
+__global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Phys &P = a.P;
   const int nb = P.nb;
@@ -437,40 +446,16 @@ __global__ void __launch_bounds__(NT_MAX, 2) rollout_kernel(const Args a) {
     const float4 *wsrc = wbuf + cur * L.capbuf;  // raw wake of this iteration (read-only)
     float4 *wk = wbuf + (cur ^ 1) * L.capbuf;    // compacted, advected wake being built
 
-    // ---------------- S1: convection sweep (+ loads sweep of step t-1)
-    float ux[R], uz[R];
-    if (conv) {
-      float ntx[R], ntz[R], bx_[R], bz_[R];
-      int kw = 0;
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const int c = tid + NT * k;
-        ntx[k] = 0.f;
-        ntz[k] = 0.f;
-        if (c < n_live) {
-          const float4 v = wsrc[raw_index(c, ctl->holes, nh)];
-          ntx[k] = -v.x;
-          ntz[k] = -v.y;
-        }
-        if (32 * warp + NT * k < n_live) kw = k + 1;
-        ux[k] = 0.f;
-        uz[k] = 0.f;
-        bx_[k] = 0.f;
-        bz_[k] = 0.f;
-      }
-      sweep_dispatch<R>(kw, wsrc, n_raw, ntx, ntz, ux, uz, rc4);
-      sweep_dispatch<R>(kw, psrc, n_prev, ntx, ntz, bx_, bz_, rc4);
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        ux[k] = -ux[k] - bx_[k];  // u_x = -(wake chain) - (bound-row chain)
-        uz[k] = uz[k] + bz_[k];
-      }
-    }
+    // ---------------- P1: wake velocity at the panels of step t-1 (its loads)
     if (pend) split_sweep(wsrc, n_raw, st, nb, rc4, red, RS, warp, lane, NW);
     __syncthreads();  // B1
 
-    // ---------------- D: loads + integration of step t-1, geometry of step t
-    if (warp == 0) {
+    // P2 runs in two passes: pass D_PASS is warp 0's control work, the other the
+    // sweep + advection of every warp.
+    for (int pass = 0; pass < 2; ++pass) {
+    // ---------------- P2, control warp: D = loads + integration of step t-1,
+    //                  geometry / gates / control of step t
+    if (pass == D_PASS && warp == 0) {
       if (pend) {
         const double fx = ctl->fx, fz = ctl->fz, nx = ctl->nx, nz = ctl->nz, s = ctl->s;
         const double rx = ctl->x[0], rz = ctl->x[1], vx = ctl->x[4], vz = ctl->x[5], om = ctl->x[6];
@@ -576,21 +561,61 @@ __global__ void __launch_bounds__(NT_MAX, 2) rollout_kernel(const Args a) {
           const double u = control_at(a, row, t);
           ctl->u = clampd(u, -P.u_lim, P.u_lim);
         }
+        __syncwarp();
+        // collocation rows of step t for S2: the upstream edge point is skipped
+        // (_core.pyx:274-275)
+        const int shed_rev = ctl->shed && ctl->rev;
+        for (int i = lane; i < nb; i += 32) {
+          const int ri = shed_rev ? i : i + 1;
+          st[i] = make_float2((float)cx[ri], (float)cz[ri]);
+        }
       }
     }
-
-    // ---------------- A: advect / dissipate / age into compacted slots
-    // (reads the raw buffer, writes the other one: no read/write race, and on a
-    //  failure in D the raw buffer still holds the reference's failure-time wake)
-    if (conv) {
+    if (pass != D_PASS && conv) {
+      // ---------------- P2, all warps: S1 convection sweep of step t, then A
+      // (reads the raw buffer, writes the other one: no read/write race with
+      //  the warps still sweeping, and on a failure in D the raw buffer still
+      //  holds the reference's failure-time wake).  Slot k of warp w holds the
+      //  particles c = 32 (NW k + w) + lane; warp 0 takes its slots after D.
+      const int kmax = R;
+      auto slot_base = [&](int k) { return 32 * (NW * k + warp); };
+      float ux[R], uz[R];
+      {
+        float ntx[R], ntz[R], bx_[R], bz_[R];
+        int kw = 0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          const int c = slot_base(k) + lane;
+          ntx[k] = 0.f;
+          ntz[k] = 0.f;
+          if (k < kmax && c < n_live) {
+            const float4 v = wsrc[raw_index(c, ctl->holes, nh)];
+            ntx[k] = -v.x;
+            ntz[k] = -v.y;
+          }
+          if (k < kmax && slot_base(k) < n_live) kw = k + 1;
+          ux[k] = 0.f;
+          uz[k] = 0.f;
+          bx_[k] = 0.f;
+          bz_[k] = 0.f;
+        }
+        sweep_dispatch<R>(kw, wsrc, n_raw, ntx, ntz, ux, uz, rc4);
+        sweep_dispatch<R>(kw, psrc, n_prev, ntx, ntz, bx_, bz_, rc4);
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          ux[k] = -ux[k] - bx_[k];  // u_x = -(wake chain) - (bound-row chain)
+          uz[k] = uz[k] + bz_[k];
+        }
+      }
+      // A: advect / dissipate / age into the compacted slot c (_core.pyx:222-226)
       const int ra = ctl->ring_a, rb = ctl->ring_b;
       unsigned keys[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        const int c = tid + NT * k;
+        const int c = slot_base(k) + lane;
         keys[k] = 0u;
         double g = 0.0;
-        if (c < n_live) {
+        if (k < kmax && c < n_live) {
           const float4 v = wsrc[raw_index(c, ctl->holes, nh)];
           const float nxp = (float)((double)v.x + dt * (double)ux[k]);
           const float nzp = (float)((double)v.y + dt * (double)uz[k]);
@@ -600,10 +625,10 @@ __global__ void __launch_bounds__(NT_MAX, 2) rollout_kernel(const Args a) {
           g = (double)ng;
           if (c != ra && c != rb) keys[k] = ((unsigned)(na + 1) << 12) | (unsigned)(4095 - c);
         }
-        // Kelvin sum over the canonical 32-particle block c / 32 = warp + NW k
-        if (32 * warp + NT * k < n_live) {
+        // Kelvin sum over the canonical 32-particle block c / 32
+        if (k < kmax && slot_base(k) < n_live) {
           g = warp_sum_d(g);
-          if (lane == 0) kblk[warp + NW * k] = g;
+          if (lane == 0) kblk[slot_base(k) >> 5] = g;
         }
       }
       const int mc = ctl->mcnt;
@@ -622,20 +647,12 @@ __global__ void __launch_bounds__(NT_MAX, 2) rollout_kernel(const Args a) {
         }
       }
     }
+    }  // passes
     __syncthreads();  // B2
     if (!conv || ctl->fail) break;
 
     // ---------------- S2: wake velocity at the collocation rows of step t
-    {
-      const int shed_rev = ctl->shed && ctl->rev;
-      // rows: skip the upstream edge point (_core.pyx:274-275)
-      for (int i = tid; i < nb; i += NT) {
-        const int ri = shed_rev ? i : i + 1;
-        st[i] = make_float2((float)cx[ri], (float)cz[ri]);
-      }
-      __syncthreads();
-      split_sweep(wk, n_live, st, nb, rc4, red, RS, warp, lane, NW);
-    }
+    split_sweep(wk, n_live, st, nb, rc4, red, RS, warp, lane, NW);
     __syncthreads();  // B3
 
     // ---------------- E: solve, shed, merge, ring termination (warp 0)
@@ -901,16 +918,25 @@ __global__ void __launch_bounds__(NTH) mppi_partial_kernel(const double *__restr
   z = warp_sum_d(z);
   if (lane == 0) sred[NW + warp] = z;
   __syncthreads();
-  // weighted control sums: warps stride over rows, lanes over steps
+  // weighted control sums: warp w takes the 32-row blocks w, w+NW, ...; the block's
+  // weights are loaded in one coalesced read and only rows with w > 0 (a handful
+  // at lambda = 0.05) are visited, in row order, lanes striding over steps
   for (int t = lane; t < T; t += 32) sacc[warp * T + t] = 0.0;
-  for (int r = warp; r < rows; r += NW) {
-    const double w = wbuf[r];
-    if (w == 0.0) continue;
-    const int g = row_begin + r;
-    for (int t = lane; t < T; t += 32) {
-      double u = ustar[t];
-      if (g > 0) u = clampd(u + noise[(size_t)(g - 1) * T + t] * sigma, -ulim, ulim);
-      sacc[warp * T + t] += w * u;
+  __syncwarp();
+  for (int base = 32 * warp; base < rows; base += 32 * NW) {
+    const int r = base + lane;
+    const double wl = r < rows ? wbuf[r] : 0.0;
+    unsigned live = __ballot_sync(0xffffffffu, wl != 0.0);
+    while (live) {
+      const int i = __ffs(live) - 1;
+      live &= live - 1;
+      const double w = __shfl_sync(0xffffffffu, wl, i);
+      const int g = row_begin + base + i;
+      for (int t = lane; t < T; t += 32) {
+        double u = ustar[t];
+        if (g > 0) u = clampd(u + noise[(size_t)(g - 1) * T + t] * sigma, -ulim, ulim);
+        sacc[warp * T + t] += w * u;
+      }
     }
   }
   __syncthreads();
