@@ -37,6 +37,8 @@ extern "C" {
 #define VPM_ERR_CONFIG (-1) /* limits / argument errors (reference: ValueError) */
 #define VPM_ERR_CUDA (-2)   /* CUDA runtime failure */
 #define VPM_ERR_ALLFAIL (-3) /* every MPPI candidate failed (mppi.py:55-56) */
+#define VPM_ERR_RANK (-4)    /* < 6 perturbed rollouts survived (policy.py:88-90) */
+#define VPM_ERR_DIVERGED (-5) /* Riccati recursion non-finite (policy.py:231-232) */
 
 /* Flattened FluidState (rollout.py:59-62 order), FP64 reference layout.
  * wake_pos is (n_wake, 2) C-order; buffers may be longer than n_wake. */
@@ -164,6 +166,39 @@ int vpm_mppi_iteration(vpm_plan *p, const double *d_x0, double *d_ustar, const d
 int vpm_mppi_optimize_host(vpm_plan *p, const double *x0, double *u_star, const double *noise,
                            int iters, int K, int T, double sigma, double temperature,
                            const double *q, const double *x_perch);
+
+/* ---- sample-built tracking controller (policy.py:66-266) ---------------------- */
+
+/* Device: per-step least-squares Jacobians of the acceleration rows over the
+ * surviving perturbed rollouts (estimate_linear_sequence, policy.py:141-171) when
+ * do_fit, then the backward Riccati gains (tvlqr_backward, policy.py:206-233) when
+ * do_riccati.  Shapes: nom_x (H+1,7), nom_u (H), cloud_x (K,H+1,7), cloud_u (K,H),
+ * status (K); a_cont (H,3,5), b_cont (H,3), a_disc (H,7,7), b_disc (H,7) (inputs
+ * when !do_fit), gains (H,7); *d_flag = 1 + step where the recursion diverged. */
+int vpm_policy_fit(const double *d_nom_x, const double *d_nom_u, const double *d_cloud_x,
+                   const double *d_cloud_u, const int64_t *d_status, int K, int H, double dt,
+                   const double *d_q_running, double r_running, const double *d_q_final,
+                   double *d_a_cont, double *d_b_cont, double *d_a_disc, double *d_b_disc,
+                   double *d_gains, int32_t *d_flag, int do_fit, int do_riccati, void *stream);
+
+/* Host buffers: build_policy (policy.py:247-266) -- K perturbed rollouts from
+ * x0s (K,7) with controls u_cloud (K,H) on plan p's fluid in one launch, then fit
+ * and Riccati.  Returns VPM_ERR_RANK (< 6 survivors) / VPM_ERR_DIVERGED like the
+ * reference's RankDeficientData / FloatingPointError.  Any output may be NULL. */
+int vpm_build_policy_host(vpm_plan *p, const double *nom_x, const double *nom_u, int H,
+                          const double *x0s, const double *u_cloud, int K, double dt,
+                          const double *q_running, double r_running, const double *q_final,
+                          double *a_cont, double *b_cont, double *a_disc, double *b_disc,
+                          double *gains, int64_t *status_out, double *cloud_x_out);
+
+/* Host buffers: estimate_linear_sequence alone (policy.py:141-171). */
+int vpm_policy_fit_host(const double *nom_x, const double *nom_u, int H, const double *cloud_x,
+                        const double *cloud_u, const int64_t *status, int K, double dt,
+                        double *a_cont, double *b_cont, double *a_disc, double *b_disc);
+
+/* Host buffers: tvlqr_backward alone (policy.py:206-233). */
+int vpm_tvlqr_host(const double *a_disc, const double *b_disc, int H, const double *q_running,
+                   double r_running, const double *q_final, double *gains);
 
 /* Average duration (ms) of the rollout kernel over the launches recorded since
  * the last reset, timed with CUDA events on the launch stream. */

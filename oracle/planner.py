@@ -123,3 +123,26 @@ def perturbed_cloud(nom_states, nom_inputs, flat_fluid, iparams, fparams, dx0_no
     d = stepper.batch_rollout_diag(x0s, U, *flat_fluid, iparams, fparams, record=True,
                                    per_rollout_x0=True)
     return d["trajs"], U, d["status"] == 0
+
+
+def shard_partial(J, controls, temperature):
+    """Per-shard softmax partial of the sharded update (paper_2509_16079_b200/sharding.py):
+    (J_min_r, Z_r, S_r) over this shard's rows; J_min_r = inf when none is finite."""
+    J = np.asarray(J, float)
+    ok = np.isfinite(J)
+    H = np.asarray(controls).shape[1]
+    if not ok.any():
+        return np.concatenate([[np.inf, 0.0], np.zeros(H)])
+    jm = J[ok].min()
+    w = np.where(ok, np.exp(-(J - jm) / temperature), 0.0)
+    return np.concatenate([[jm, w.sum()], (w[:, None] * np.asarray(controls, float)).sum(axis=0)])
+
+
+def combine_partials(parts, temperature):
+    """Rank-ordered combine of gathered partials: rescale to the global J_min."""
+    parts = np.asarray(parts, float)
+    jm = parts[:, 0].min()
+    if not np.isfinite(jm):
+        raise ValueError("all sampled rollouts failed (infinite cost)")
+    e = np.where(np.isfinite(parts[:, 0]), np.exp(-(parts[:, 0] - jm) / temperature), 0.0)
+    return (e[:, None] * parts[:, 2:]).sum(axis=0) / (e * parts[:, 1]).sum()

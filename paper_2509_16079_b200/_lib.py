@@ -23,7 +23,8 @@ SOURCES = [os.path.join(PKG, "csrc", "vpm_capi.cu"), os.path.join(PKG, "csrc", "
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17", "-fmad=false",
               "-shared", "-Xcompiler", "-fPIC"]
 
-VPM_OK, VPM_ERR_CONFIG, VPM_ERR_CUDA, VPM_ERR_ALLFAIL = 0, -1, -2, -3
+VPM_OK, VPM_ERR_CONFIG, VPM_ERR_CUDA, VPM_ERR_ALLFAIL, VPM_ERR_RANK, VPM_ERR_DIVERGED = (
+    0, -1, -2, -3, -4, -5)
 
 
 class CudaBackendError(RuntimeError):
@@ -121,6 +122,14 @@ def lib():
             "vpm_fp32_peak_probe": (C.c_double, [C.c_int, C.c_int]),
             "vpm_launch_shape": (C.c_int, [C.c_int, C.c_int, C.c_int, _I32, _I32, _I32]),
             "vpm_boundary_inverse": (C.c_int, [_I64, _D, _D]),
+            "vpm_policy_fit": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_double, vp,
+                                         C.c_double, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int,
+                                         vp]),
+            "vpm_build_policy_host": (C.c_int, [vp, _D, _D, C.c_int, _D, _D, C.c_int, C.c_double,
+                                                _D, C.c_double, _D, _D, _D, _D, _D, _D, _I64, _D]),
+            "vpm_policy_fit_host": (C.c_int, [_D, _D, C.c_int, _D, _D, _I64, C.c_int, C.c_double,
+                                              _D, _D, _D, _D]),
+            "vpm_tvlqr_host": (C.c_int, [_D, _D, C.c_int, _D, C.c_double, _D, _D]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -134,7 +143,8 @@ EXPORTED = ("vpm_step", "vpm_rollout", "vpm_batch_rollout", "vpm_batch_rollout_x
             "vpm_last_error", "vpm_plan_create", "vpm_plan_destroy", "vpm_plan_set_fluid",
             "vpm_plan_batch", "vpm_mppi_partial", "vpm_mppi_combine", "vpm_mppi_iteration",
             "vpm_mppi_optimize_host", "vpm_plan_timing", "vpm_fp32_peak_probe", "vpm_launch_shape",
-            "vpm_boundary_inverse")
+            "vpm_boundary_inverse", "vpm_policy_fit", "vpm_build_policy_host",
+            "vpm_policy_fit_host", "vpm_tvlqr_host")
 
 
 def last_error() -> str:
@@ -150,6 +160,11 @@ def check(rc: int, what: str) -> int:
         raise ValueError(msg)
     if rc == VPM_ERR_ALLFAIL:
         raise ValueError("all sampled rollouts failed (infinite cost)")
+    if rc == VPM_ERR_RANK:
+        from .policy import RankDeficientData
+        raise RankDeficientData(last_error())
+    if rc == VPM_ERR_DIVERGED:
+        raise FloatingPointError(last_error())
     raise CudaBackendError(msg)
 
 

@@ -800,4 +800,166 @@ int vpm_batch_rollout_x0(const double *x0, const double *controls, int B, int T,
                   trajs, nullptr, nullptr, nullptr);
 }
 
+// ---- sample-built tracking controller ---------------------------------------------
+int vpm_policy_fit(const double *d_nom_x, const double *d_nom_u, const double *d_cloud_x,
+                   const double *d_cloud_u, const int64_t *d_status, int K, int H, double dt,
+                   const double *d_q_running, double r_running, const double *d_q_final,
+                   double *d_a_cont, double *d_b_cont, double *d_a_disc, double *d_b_disc,
+                   double *d_gains, int32_t *d_flag, int do_fit, int do_riccati, void *stream) {
+  if (H < 0 || K < 0 || dt <= 0.0) return fail_cfg("bad policy shape");
+  if (H == 0) return VPM_OK;
+  vpm::PolicyArgs a;
+  a.nom_x = d_nom_x;
+  a.nom_u = d_nom_u;
+  a.cx = d_cloud_x;
+  a.cu = d_cloud_u;
+  a.status = d_status;
+  a.K = K;
+  a.H = H;
+  a.dt = dt;
+  a.qr = d_q_running;
+  a.qf = d_q_final;
+  a.r = r_running;
+  a.a_cont = d_a_cont;
+  a.b_cont = d_b_cont;
+  a.a_disc = d_a_disc;
+  a.b_disc = d_b_disc;
+  a.gains = d_gains;
+  a.flag = d_flag;
+  a.do_fit = do_fit;
+  a.do_riccati = do_riccati;
+  vpm::policy_kernel<<<1, 512, 0, (cudaStream_t)stream>>>(a);
+  CK(cudaGetLastError());
+  return VPM_OK;
+}
+
+namespace {
+// Host-buffer driver of the controller: optional perturbed rollouts on a plan, then
+// the fit / Riccati kernel.  Outputs are copied back when their pointers are set.
+int policy_host(vpm_plan *p, const double *nom_x, const double *nom_u, int H, const double *x0s,
+                const double *u_cloud, const double *cloud_x_in, const int64_t *status_in, int K,
+                double dt, const double *q_running, double r_running, const double *q_final,
+                const double *a_disc_in, const double *b_disc_in, double *a_cont, double *b_cont,
+                double *a_disc, double *b_disc, double *gains, int64_t *status_out,
+                double *cloud_x_out, int do_fit, int do_riccati) {
+  if (H < 0 || K < 0) return fail_cfg("negative horizon or sample count");
+  if (do_fit && x0s && !p) return fail_cfg("a plan is required for the perturbed rollouts");
+  if (H == 0) return VPM_OK;
+  int dev = 0;
+  if (p) {
+    CK(cudaSetDevice(p->device));
+    dev = p->device;
+  } else {
+    CK(cudaGetDevice(&dev));
+  }
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const size_t nx = (size_t)K * (H + 1) * 7;
+  const size_t need = 16 * 256 + sizeof(double) * ((H + 1) * 7 + H + nx + (size_t)K * H + (size_t)K * 7 +
+                                                  14 + H * (15 + 3 + 49 + 7 + 7)) +
+                      sizeof(int64_t) * K + 64;
+  void *buf = nullptr;
+  CK(cudaMallocAsync(&buf, need, st));
+  Carve cv{(char *)buf};
+  double *d_nx = cv.take<double>((size_t)(H + 1) * 7), *d_nu = cv.take<double>(H + 1);
+  double *d_cx = cv.take<double>(nx + 1), *d_cu = cv.take<double>((size_t)K * H + 1);
+  double *d_x0 = cv.take<double>((size_t)K * 7 + 1), *d_q = cv.take<double>(7), *d_qf = cv.take<double>(7);
+  double *d_ac = cv.take<double>((size_t)H * 15 + 1), *d_bc = cv.take<double>((size_t)H * 3 + 1);
+  double *d_ad = cv.take<double>((size_t)H * 49 + 1), *d_bd = cv.take<double>((size_t)H * 7 + 1);
+  double *d_g = cv.take<double>((size_t)H * 7 + 1);
+  int64_t *d_st = cv.take<int64_t>(K + 1);
+  int32_t *d_flag = cv.take<int32_t>(4);
+  int rc = VPM_OK;
+  if (do_fit) {
+    CK(cudaMemcpyAsync(d_nx, nom_x, sizeof(double) * (H + 1) * 7, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_nu, nom_u, sizeof(double) * H, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemcpyAsync(d_q, q_running, sizeof(double) * 7, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_qf, q_final, sizeof(double) * 7, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_flag, 0, 16, st));
+  if (do_fit) {
+    CK(cudaMemcpyAsync(d_cu, u_cloud, sizeof(double) * K * H, cudaMemcpyHostToDevice, st));
+    if (x0s) {  // perturbed rollouts on the device (policy.py:66-91), one launch
+      CK(cudaMemcpyAsync(d_x0, x0s, sizeof(double) * K * 7, cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(d_cx, 0, sizeof(double) * nx, st));
+      vpm_batch_out o;
+      std::memset(&o, 0, sizeof(o));
+      o.status = d_st;
+      o.trajs = d_cx;
+      rc = vpm_plan_batch(p, d_x0, 7, d_cu, nullptr, nullptr, 0.0, 0, K, H, nullptr, nullptr, 1, &o, st);
+    } else {
+      CK(cudaMemcpyAsync(d_cx, cloud_x_in, sizeof(double) * nx, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(d_st, status_in, sizeof(int64_t) * K, cudaMemcpyHostToDevice, st));
+    }
+  } else {
+    CK(cudaMemcpyAsync(d_ad, a_disc_in, sizeof(double) * H * 49, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_bd, b_disc_in, sizeof(double) * H * 7, cudaMemcpyHostToDevice, st));
+  }
+  int64_t survivors = K;
+  if (rc == VPM_OK && do_fit && x0s) {
+    std::vector<int64_t> sv(K > 0 ? K : 1);
+    CK(cudaMemcpyAsync(sv.data(), d_st, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    survivors = 0;
+    for (int i = 0; i < K; ++i) survivors += sv[i] == 0;
+    if (status_out) std::memcpy(status_out, sv.data(), sizeof(int64_t) * K);
+    if (survivors < 6) {
+      g_err = "only " + std::to_string(survivors) + " of " + std::to_string(K) +
+              " perturbed rollouts survived";
+      rc = VPM_ERR_RANK;
+    }
+  }
+  if (rc == VPM_OK && (do_fit || do_riccati))
+    rc = vpm_policy_fit(d_nx, d_nu, d_cx, d_cu, d_st, K, H, dt, d_q, r_running, d_qf, d_ac, d_bc,
+                        d_ad, d_bd, d_g, d_flag, do_fit, do_riccati, st);
+  int32_t flag[4] = {0, 0, 0, 0};
+  if (rc == VPM_OK) {
+    if (a_cont && do_fit) CK(cudaMemcpyAsync(a_cont, d_ac, sizeof(double) * H * 15, cudaMemcpyDeviceToHost, st));
+    if (b_cont && do_fit) CK(cudaMemcpyAsync(b_cont, d_bc, sizeof(double) * H * 3, cudaMemcpyDeviceToHost, st));
+    if (a_disc && do_fit) CK(cudaMemcpyAsync(a_disc, d_ad, sizeof(double) * H * 49, cudaMemcpyDeviceToHost, st));
+    if (b_disc && do_fit) CK(cudaMemcpyAsync(b_disc, d_bd, sizeof(double) * H * 7, cudaMemcpyDeviceToHost, st));
+    if (gains && do_riccati) CK(cudaMemcpyAsync(gains, d_g, sizeof(double) * H * 7, cudaMemcpyDeviceToHost, st));
+    if (cloud_x_out && do_fit) CK(cudaMemcpyAsync(cloud_x_out, d_cx, sizeof(double) * nx, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(flag, d_flag, sizeof(flag), cudaMemcpyDeviceToHost, st));
+  }
+  cudaFreeAsync(buf, st);
+  CK(cudaStreamSynchronize(st));
+  CK(cudaStreamDestroy(st));
+  (void)dev;
+  if (rc) return rc;
+  if (do_riccati && flag[0]) {
+    g_err = "Riccati recursion diverged at step " + std::to_string(flag[0] - 1);
+    return VPM_ERR_DIVERGED;
+  }
+  return VPM_OK;
+}
+}  // namespace
+
+int vpm_build_policy_host(vpm_plan *p, const double *nom_x, const double *nom_u, int H,
+                          const double *x0s, const double *u_cloud, int K, double dt,
+                          const double *q_running, double r_running, const double *q_final,
+                          double *a_cont, double *b_cont, double *a_disc, double *b_disc,
+                          double *gains, int64_t *status_out, double *cloud_x_out) {
+  return policy_host(p, nom_x, nom_u, H, x0s, u_cloud, nullptr, nullptr, K, dt, q_running, r_running,
+                     q_final, nullptr, nullptr, a_cont, b_cont, a_disc, b_disc, gains, status_out,
+                     cloud_x_out, 1, 1);
+}
+
+int vpm_policy_fit_host(const double *nom_x, const double *nom_u, int H, const double *cloud_x,
+                        const double *cloud_u, const int64_t *status, int K, double dt,
+                        double *a_cont, double *b_cont, double *a_disc, double *b_disc) {
+  const double zero7[7] = {0, 0, 0, 0, 0, 0, 0};
+  return policy_host(nullptr, nom_x, nom_u, H, nullptr, cloud_u, cloud_x, status, K, dt, zero7, 1.0,
+                     zero7, nullptr, nullptr, a_cont, b_cont, a_disc, b_disc, nullptr, nullptr,
+                     nullptr, 1, 0);
+}
+
+int vpm_tvlqr_host(const double *a_disc, const double *b_disc, int H, const double *q_running,
+                   double r_running, const double *q_final, double *gains) {
+  const double zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  return policy_host(nullptr, zero, zero, H, nullptr, nullptr, nullptr, nullptr, 0, 1.0, q_running,
+                     r_running, q_final, a_disc, b_disc, nullptr, nullptr, nullptr, nullptr, gains,
+                     nullptr, nullptr, 0, 1);
+}
+
 }  // extern "C"

@@ -14,23 +14,25 @@
 //   terminal cost     mppi.py:28-34
 //   MPPI update       mppi.py:46-59
 //
-// Per-step phase schedule inside the CTA (barriers B1..B4):
+// Per-step phase schedule inside the CTA (barriers B1..B4), iteration t:
 //
-//   S1  all threads: velocity at every live wake particle from every wake
-//       particle + the previous bound row (convection of step t, _core.pyx:192-221)
-//       and, source-split, the wake velocity at the panels of step t-1 (the loads
-//       of step t-1, _core.pyx:385-389 -- same sources: the post-merge wake).
+//   P1  all warps, source-split: wake velocity at the panels of step t-1 (the
+//       loads of step t-1, _core.pyx:385-389; the sources are the post-merge wake,
+//       i.e. exactly the sources of the convection sweep of step t).
 //   B1
-//   D   warp 0: unsteady-Bernoulli loads of step t-1 (_core.pyx:375-418),
-//       elevator + Euler integration (_core.pyx:423-461), envelope check
-//       (_core.pyx:483-484), then the chord frame / collocation geometry and the
-//       stall + reversed-flow gates of step t (_core.pyx:228-256).
-//   A   all threads (overlapping D): Euler advection, dissipation, ageing of
-//       their own particles (_core.pyx:222-226), read from the raw buffer and
-//       written compacted into the other buffer (this retires the ordered
-//       removals of step t-1); Kelvin block sums; per-warp merge candidates.
+//   P2  warp 0 first runs D: unsteady-Bernoulli loads of step t-1
+//       (_core.pyx:375-418), elevator + Euler integration (_core.pyx:423-461),
+//       envelope check (_core.pyx:483-484), then the chord frame / collocation
+//       geometry, gates and control of step t (_core.pyx:228-256).
+//       All warps: S1 = velocity at every live wake particle from every wake
+//       particle + the previous bound row (convection, _core.pyx:192-221), register
+//       tiled; then A = Euler advection, dissipation, ageing (_core.pyx:222-226),
+//       read from the raw buffer and written compacted into the other buffer
+//       (this retires the ordered removals of step t-1); Kelvin block sums;
+//       per-warp merge candidates.
 //   B2
-//   S2  all threads: wake velocity at the nb collocation rows (_core.pyx:273-296).
+//   S2  all warps, source-split: wake velocity at the nb collocation rows
+//       (_core.pyx:273-296).
 //   B3
 //   E   warp 0: right-hand side, bound-circulation solve with the precomputed
 //       inverse of the pose-invariant system, shed LEV/TEV
@@ -918,26 +920,40 @@ __global__ void __launch_bounds__(NTH) mppi_partial_kernel(const double *__restr
   z = warp_sum_d(z);
   if (lane == 0) sred[NW + warp] = z;
   __syncthreads();
-  // weighted control sums: warp w takes the 32-row blocks w, w+NW, ...; the block's
-  // weights are loaded in one coalesced read and only rows with w > 0 (a handful
-  // at lambda = 0.05) are visited, in row order, lanes striding over steps
-  for (int t = lane; t < T; t += 32) sacc[warp * T + t] = 0.0;
-  __syncwarp();
-  for (int base = 32 * warp; base < rows; base += 32 * NW) {
-    const int r = base + lane;
-    const double wl = r < rows ? wbuf[r] : 0.0;
-    unsigned live = __ballot_sync(0xffffffffu, wl != 0.0);
-    while (live) {
-      const int i = __ffs(live) - 1;
-      live &= live - 1;
-      const double w = __shfl_sync(0xffffffffu, wl, i);
-      const int g = row_begin + base + i;
-      for (int t = lane; t < T; t += 32) {
-        double u = ustar[t];
-        if (g > 0) u = clampd(u + noise[(size_t)(g - 1) * T + t] * sigma, -ulim, ulim);
-        sacc[warp * T + t] += w * u;
+  // weighted control sums S[t] = sum_r w_r u_r[t]: warp w takes the 32-row blocks
+  // w, w+NW, ... in row order; lanes own steps t = tc + lane, tc + 32 + lane with
+  // the accumulators in registers; 8 rows' control loads are in flight at once
+  // (rows with w = 0 load nothing and add an exact 0)
+  for (int tc = 0; tc < T; tc += 64) {
+    const int t0 = tc + lane, t1 = tc + 32 + lane;
+    const double us0 = t0 < T ? ustar[t0] : 0.0, us1 = t1 < T ? ustar[t1] : 0.0;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int base = 32 * warp; base < rows; base += 32 * NW) {
+      const int r = base + lane;
+      const double wl = r < rows ? wbuf[r] : 0.0;
+      for (int i = 0; i < 32; i += 8) {
+        double w[8], u0[8], u1[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          w[j] = __shfl_sync(0xffffffffu, wl, i + j);
+          const int g = row_begin + base + i + j;
+          u0[j] = us0;
+          u1[j] = us1;
+          if (w[j] != 0.0 && g > 0) {
+            const double *nz = noise + (size_t)(g - 1) * T;
+            if (t0 < T) u0[j] = clampd(us0 + nz[t0] * sigma, -ulim, ulim);
+            if (t1 < T) u1[j] = clampd(us1 + nz[t1] * sigma, -ulim, ulim);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc0 += w[j] * u0[j];
+          acc1 += w[j] * u1[j];
+        }
       }
     }
+    if (t0 < T) sacc[warp * T + t0] = acc0;
+    if (t1 < T) sacc[warp * T + t1] = acc1;
   }
   __syncthreads();
   if (tid == 0) {
@@ -977,6 +993,213 @@ __global__ void mppi_combine_kernel(const double *__restrict__ parts, int W, int
     ustar[t] = S / Z;
   }
   if (threadIdx.x == 0 && flag) *flag = 0;
+}
+
+// ---- sample-built TVLQR tracking controller (policy.py:121-233) ----------------------
+struct PolicyArgs {
+  const double *nom_x, *nom_u;      // (H+1, 7), (H)
+  const double *cx, *cu;            // perturbed cloud: (K, H+1, 7), (K, H)
+  const int64_t *status;            // (K) 0 = survived
+  int K, H;
+  double dt;
+  const double *qr, *qf;            // (7) diagonal running / final weights
+  double r;
+  double *a_cont, *b_cont;          // (H, 3, 5), (H, 3)
+  double *a_disc, *b_disc;          // (H, 7, 7), (H, 7)  (inputs when !do_fit)
+  double *gains;                    // (H, 7)
+  int32_t *flag;                    // [0]: 1 + step where Riccati diverged, 0 ok
+  int do_fit, do_riccati;
+};
+
+// regressor state columns theta, phi, v_x, v_z, omega = 2..6 (policy.py:28)
+__device__ __forceinline__ int reg_col(int c) { return c + 2; }
+
+__device__ __forceinline__ void cloud_row(const PolicyArgs &p, int i, int k, const double *nk,
+                                          const double *nk1, double z[6], double y[3]) {
+  const double *s0 = p.cx + ((size_t)i * (p.H + 1) + k) * 7;
+  const double *s1 = s0 + 7;
+#pragma unroll
+  for (int c = 0; c < 5; ++c) z[c] = s0[reg_col(c)] - nk[reg_col(c)];
+  z[5] = p.cu[(size_t)i * p.H + k] - p.nom_u[k];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    y[r] = (s1[4 + r] - s0[4 + r]) / p.dt - (nk1[4 + r] - nk[4 + r]) / p.dt;
+}
+
+// Phase 1, one warp per step k: least squares of the acceleration rows (v_x, v_z,
+// omega derivatives) on the 6 regressors over the surviving rollouts
+// (estimate_linear_sequence, policy.py:141-171).  Columns with norm <= 1e-10 x the
+// largest are dropped (their Jacobian entries stay 0); the others are scaled to
+// unit norm, the normal equations are accumulated with warp reductions in FP64 and
+// solved by Cholesky (the scaling keeps the squared condition number small; SURVEY
+// 7.3.6).  Euler discretisation with the analytic kinematic rows
+// (assemble_discrete, policy.py:121-138).
+// Phase 2, warp 0: backward Riccati recursion S_N = Q_f, h_k = (b'S A)/(r + b'S b),
+// S <- Q + A'S A - (A'S b) h', symmetrised (tvlqr_backward, policy.py:206-233).
+__global__ void __launch_bounds__(512) policy_kernel(const PolicyArgs p) {
+  __shared__ double S[49], SA[49], A[49], Sn[49], bv[7], Sb[7], bS[7], AtSb[7], hh[7];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  if (p.do_fit) {
+    for (int k = warp; k < p.H; k += NW) {
+      const double *nk = p.nom_x + (size_t)k * 7, *nk1 = nk + 7;
+      double n2[6] = {0, 0, 0, 0, 0, 0};
+      for (int i = lane; i < p.K; i += 32) {
+        if (p.status[i] != 0) continue;
+        double z[6], y[3];
+        cloud_row(p, i, k, nk, nk1, z, y);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) n2[c] += z[c] * z[c];
+      }
+      double nrm[6], mx = 0.0;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        nrm[c] = sqrt(warp_sum_d(n2[c]));
+        mx = fmax(mx, nrm[c]);
+      }
+      const double thr = 1e-10 * fmax(mx, 1e-30);
+      double G[21], Rg[18];
+#pragma unroll
+      for (int e = 0; e < 21; ++e) G[e] = 0.0;
+#pragma unroll
+      for (int e = 0; e < 18; ++e) Rg[e] = 0.0;
+      for (int i = lane; i < p.K; i += 32) {
+        if (p.status[i] != 0) continue;
+        double z[6], y[3];
+        cloud_row(p, i, k, nk, nk1, z, y);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) z[c] = nrm[c] > thr ? z[c] / nrm[c] : 0.0;
+        int e = 0;
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+#pragma unroll
+          for (int b = a; b < 6; ++b) G[e++] += z[a] * z[b];
+#pragma unroll
+          for (int r = 0; r < 3; ++r) Rg[a * 3 + r] += z[a] * y[r];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 21; ++e) G[e] = warp_sum_d(G[e]);
+#pragma unroll
+      for (int e = 0; e < 18; ++e) Rg[e] = warp_sum_d(Rg[e]);
+      if (lane == 0) {
+        // Cholesky of the active block (inactive columns: unit diagonal, zero rhs)
+        double L[36], x[18];
+        int e = 0;
+        for (int a = 0; a < 6; ++a)
+          for (int b = a; b < 6; ++b, ++e) {
+            const bool act = nrm[a] > thr && nrm[b] > thr;
+            L[b * 6 + a] = L[a * 6 + b] = act ? G[e] : (a == b ? 1.0 : 0.0);
+          }
+        for (int a = 0; a < 6; ++a)
+          for (int r = 0; r < 3; ++r) x[a * 3 + r] = nrm[a] > thr ? Rg[a * 3 + r] : 0.0;
+        for (int j = 0; j < 6; ++j) {
+          double d = L[j * 6 + j];
+          for (int m = 0; m < j; ++m) d -= L[j * 6 + m] * L[j * 6 + m];
+          const bool dep = !(d > 1e-24);  // collinear excitation: drop the column
+          d = dep ? 1.0 : sqrt(d);
+          L[j * 6 + j] = d;
+          for (int i2 = j + 1; i2 < 6; ++i2) {
+            double v = L[i2 * 6 + j];
+            for (int m = 0; m < j; ++m) v -= L[i2 * 6 + m] * L[j * 6 + m];
+            L[i2 * 6 + j] = dep ? 0.0 : v / d;
+          }
+          if (dep)
+            for (int r = 0; r < 3; ++r) x[j * 3 + r] = 0.0;
+        }
+        for (int r = 0; r < 3; ++r) {  // forward then backward substitution
+          for (int j = 0; j < 6; ++j) {
+            double v = x[j * 3 + r];
+            for (int m = 0; m < j; ++m) v -= L[j * 6 + m] * x[m * 3 + r];
+            x[j * 3 + r] = v / L[j * 6 + j];
+          }
+          for (int j = 5; j >= 0; --j) {
+            double v = x[j * 3 + r];
+            for (int m = j + 1; m < 6; ++m) v -= L[m * 6 + j] * x[m * 3 + r];
+            x[j * 3 + r] = v / L[j * 6 + j];
+          }
+        }
+        double *ac = p.a_cont + (size_t)k * 15, *bc = p.b_cont + (size_t)k * 3;
+        double *ad = p.a_disc + (size_t)k * 49, *bd = p.b_disc + (size_t)k * 7;
+        for (int e2 = 0; e2 < 49; ++e2) ad[e2] = (e2 % 8 == 0) ? 1.0 : 0.0;
+        for (int e2 = 0; e2 < 7; ++e2) bd[e2] = 0.0;
+        ad[0 * 7 + 4] = p.dt;
+        ad[1 * 7 + 5] = p.dt;
+        ad[2 * 7 + 6] = p.dt;
+        bd[3] = p.dt;
+        for (int r = 0; r < 3; ++r) {
+          for (int c = 0; c < 6; ++c) {
+            const double jv = nrm[c] > thr ? x[c * 3 + r] / nrm[c] : 0.0;
+            if (c < 5) {
+              ac[r * 5 + c] = jv;
+              ad[(4 + r) * 7 + reg_col(c)] += p.dt * jv;
+            } else {
+              bc[r] = jv;
+              bd[4 + r] = p.dt * jv;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!p.do_riccati || warp != 0) return;
+  for (int e = lane; e < 49; e += 32) S[e] = (e % 8 == 0) ? p.qf[e / 7] : 0.0;
+  if (lane == 0) p.flag[0] = 0;
+  __syncwarp();
+  for (int k = p.H - 1; k >= 0; --k) {
+    for (int e = lane; e < 49; e += 32) A[e] = p.a_disc[(size_t)k * 49 + e];
+    if (lane < 7) bv[lane] = p.b_disc[(size_t)k * 7 + lane];
+    __syncwarp();
+    if (lane < 7) {
+      double s1 = 0.0, s2 = 0.0;
+      for (int j = 0; j < 7; ++j) {
+        s1 += S[lane * 7 + j] * bv[j];  // (S b)_i
+        s2 += bv[j] * S[j * 7 + lane];  // (b' S)_j
+      }
+      Sb[lane] = s1;
+      bS[lane] = s2;
+    }
+    for (int e = lane; e < 49; e += 32) {
+      const int i = e / 7, j = e % 7;
+      double v = 0.0;
+      for (int m = 0; m < 7; ++m) v += S[i * 7 + m] * A[m * 7 + j];
+      SA[e] = v;
+    }
+    __syncwarp();
+    double denom = p.r;
+    for (int i = 0; i < 7; ++i) denom += bv[i] * Sb[i];
+    if (lane < 7) {
+      double v = 0.0, w = 0.0;
+      for (int i = 0; i < 7; ++i) {
+        v += bS[i] * A[i * 7 + lane];
+        w += A[i * 7 + lane] * Sb[i];
+      }
+      hh[lane] = v / denom;
+      AtSb[lane] = w;
+      p.gains[(size_t)k * 7 + lane] = v / denom;
+    }
+    __syncwarp();
+    for (int e = lane; e < 49; e += 32) {
+      const int i = e / 7, j = e % 7;
+      double v = 0.0;
+      for (int m = 0; m < 7; ++m) v += A[m * 7 + i] * SA[m * 7 + j];
+      Sn[e] = (i == j ? p.qr[i] : 0.0) + v - AtSb[i] * hh[j];
+    }
+    __syncwarp();
+    bool fin = true;
+    for (int e = lane; e < 49; e += 32) {
+      const int i = e / 7, j = e % 7;
+      const double v = 0.5 * (Sn[i * 7 + j] + Sn[j * 7 + i]);
+      S[e] = v;
+      fin = fin && isfinite(v);
+    }
+    fin = __all_sync(0xffffffffu, fin);
+    __syncwarp();
+    if (!fin) {
+      if (lane == 0) p.flag[0] = 1 + k;
+      return;
+    }
+  }
 }
 
 // Pipe throughput probes, 8 independent chains per thread.

@@ -34,8 +34,12 @@ def gather_partials(partial, group=None):
     import torch
     import torch.distributed as dist
     W = dist.get_world_size(group)
-    out = torch.empty((W, partial.numel()), dtype=partial.dtype, device=partial.device)
-    dist.all_gather_into_tensor(out, partial.contiguous().view(-1), group=group)
+    flat = partial.contiguous().view(-1)
+    out = torch.empty((W, flat.numel()), dtype=partial.dtype, device=partial.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, flat, group=group)   # one NCCL all-gather
+    else:
+        dist.all_gather(list(out.unbind(0)), flat, group=group)
     return out
 
 

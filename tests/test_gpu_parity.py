@@ -215,6 +215,24 @@ def test_policy_C2_golden(torch_cuda):
     assert_close(pol.gains, g["gains"], rtol=2e-2, what="gains")
 
 
+def test_policy_kernels_on_reference_cloud(torch_cuda):
+    """The device regression + Riccati on the reference's own perturbed cloud
+    (identical inputs): FP64 normal equations with column scaling vs LAPACK gelsd."""
+    from paper_2509_16079_b200 import policy
+    g = golden("policy_C2.npz")
+    nom = policy.NominalTrajectory(states=g["nominal_states"], inputs=g["nominal_inputs"], dt=0.01)
+    # the reference's inputs for the cloud: clip(nominal + du * 0.5)
+    U = np.clip(g["nominal_inputs"][None, :] + g["du"] * 0.5, -15, 15)
+    seq = policy.estimate_linear_sequence(nom, g["cloud_states"], U, g["cloud_ok"], 0.01)
+    np.testing.assert_allclose(seq.a_discrete, g["a_discrete"], rtol=1e-7, atol=1e-9)
+    np.testing.assert_allclose(seq.b_discrete, g["b_discrete"], rtol=1e-7, atol=1e-9)
+    K = policy.tvlqr_backward(g["a_discrete"], g["b_discrete"], [0.1, 0.1, 5.0, 0.1, 0.1, 0.1, 5.0],
+                              0.01, [400.0, 400.0, 10.0, 1.0, 1.0, 1.0, 1.0])
+    np.testing.assert_allclose(K, g["gains"], rtol=1e-9, atol=1e-9)
+    with pytest.raises(FloatingPointError):
+        policy.tvlqr_backward(g["a_discrete"] * 1e200, g["b_discrete"], [1] * 7, 0.01, [1] * 7)
+
+
 # ------------------------------------------------------------------ full-size properties
 def test_c4_full_batch_properties(torch_cuda, oracle_core):
     """K=4096, H=50, N=512 + ring: deterministic, row-independent (batch ==
