@@ -177,6 +177,93 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------ GPU arm
+def _time_ms(torch, fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b))
+    return best
+
+
+def extras(torch, dev, sc, flat, plan, mp):
+    """Side measurements (not the headline): the C2 latency config, policy
+    synthesis on the C4 snapshot, and the C5 Biot-Savart stress sweep."""
+    from paper_2509_16079_b200 import config, policy, rollout, vpm
+    from paper_2509_16079_b200.device import DevicePlan
+    f64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev)
+    out = {}
+    # C2: K=256 (+1), H=50, cap 60, empty fluid -- latency-bound configuration
+    with np.load(os.path.join(ROOT, "tests", "golden", "scenario_C2.npz")) as z:
+        s2 = {k: z[k] for k in z.files}
+    p2 = DevicePlan(s2["iparams"], s2["fparams"], device=dev.index)
+    p2.set_fluid((s2["wake_pos"], s2["wake_gamma"], s2["wake_age"], 0, -1, -1, s2["prev_pos"],
+                  s2["prev_gamma"], 0, 0.0, s2["ema"]))
+    n2 = f64(np.random.default_rng(5).normal(0, 1, (256, HORIZON)))
+    sc2 = {"cost": torch.empty(257, dtype=torch.float64, device=dev),
+           "partial": torch.empty(HORIZON + 2, dtype=torch.float64, device=dev),
+           "flag": torch.zeros(1, dtype=torch.int32, device=dev)}
+    u2 = f64(np.full(HORIZON, -6.0))
+    x2 = f64(s2["x0"])
+    out["c2_iteration_ms"] = _time_ms(torch, lambda: p2.mppi_iteration(
+        x2, u2, n2, SIGMA, 257, LAMBDA, f64(Q), f64(XPERCH), sc2))
+    # policy synthesis (64 perturbed rollouts on the N=512 + ring snapshot, regression,
+    # Riccati) through the C ABI with host buffers, around the current u*
+    cfg = config.ExperimentConfig()
+    cfg.vpm.particle_cap = CAP
+    eng = rollout.Engine(cfg.vpm, cfg.glider)
+    eng._device_plan = plan
+    fl = vpm.FluidState.empty(cfg.vpm)
+    n = int(sc["n_wake"])
+    fl.wake_pos[:n], fl.wake_gamma[:n], fl.wake_age[:n] = sc["wake_pos"][:n], sc["wake_gamma"][:n], sc["wake_age"][:n]
+    fl.n_wake, fl.ring_a, fl.ring_b = n, int(sc["ring_a"]), int(sc["ring_b"])
+    fl.prev_pos[:], fl.prev_gamma[:], fl.n_prev = sc["prev_pos"], sc["prev_gamma"], int(sc["n_prev"])
+    fl.prev_lev_gamma, fl.unsteady_ema[:] = float(sc["prev_lev"]), sc["ema"]
+    u_nom = mp.ustar.cpu().numpy()
+    rc, traj, _ = eng.rollout(sc["x0"], u_nom, fl, record=True)
+    if rc == 0:
+        nom = policy.NominalTrajectory(states=traj, inputs=u_nom, dt=cfg.vpm.dt)
+        policy.build_policy(nom, fl, cfg.synthesis, eng, np.random.default_rng(0))
+        t0 = time.perf_counter()
+        for i in range(3):
+            policy.build_policy(nom, fl, cfg.synthesis, eng, np.random.default_rng(i))
+        out["policy_build_ms_e2e"] = 1e3 * (time.perf_counter() - t0) / 3
+    plan.set_fluid(flat)
+    # C5: Biot-Savart stress sweep, K=16384 rollouts, attached flow (no shedding, fixed N)
+    sweep = {}
+    rng = np.random.default_rng(11)
+    K5, H5 = 16384, 5
+    for N in (128, 256, 512, 1024, 2048):
+        v = config.VpmConfig(particle_cap=N)
+        ip, fp = config.pack_params(v, config.GliderParams())
+        p5 = DevicePlan(ip, fp, device=dev.index)
+        wp = rng.normal(0.0, 0.5, (N, 2))
+        wp[:, 0] -= 3.0  # wake behind the plate, plate at the origin
+        p5.set_fluid((wp, rng.normal(0.0, 0.05, N), np.zeros(N, np.int64), N, -1, -1,
+                      np.zeros((10, 2)), np.zeros(10), 0, 0.0, np.zeros(10)))
+        x5 = f64([0.0, 0.0, 0.0, 0.0, 7.0, 0.0, 0.0])
+        ctrl = torch.zeros(K5, H5, dtype=torch.float64, device=dev)
+        o5 = {"status": torch.empty(K5, dtype=torch.int64, device=dev),
+              "finals": torch.empty(K5, 7, dtype=torch.float64, device=dev),
+              "interactions": torch.zeros(K5, dtype=torch.int64, device=dev)}
+        ms = _time_ms(torch, lambda: p5.batch(x5, H5, controls=ctrl, rows=K5, out=o5))
+        inter = float(o5["interactions"].sum().item())
+        shed = int((o5["status"] != 0).sum().item())
+        sweep[str(N)] = {"ms": ms, "interactions": inter,
+                         "gflops": 12.0 * inter / (ms * 1e-3) / 1e9,
+                         "frac_of_fp32_peak": 12.0 * inter / (ms * 1e-3) / 1e12 / FP32_SPEC_TFLOPS,
+                         "failed_rollouts": shed}
+    out["c5_biot_savart_sweep"] = {"K": K5, "H": H5, "by_N": sweep,
+                                   "note": "random wake pos~N(0,0.5^2), Gamma~N(0,0.05^2), "
+                                           "attached flow; 12 flop per directed interaction"}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -317,6 +404,8 @@ def run_ours(args):
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if world == 1 and not args.no_extras:
+        line["extras"] = extras(torch, dev, sc, flat, plan, mp)
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(sc, flat)
     print(json.dumps(line), flush=True)
@@ -331,6 +420,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the C2 / policy / C5 Biot-Savart sweep side measurements")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
