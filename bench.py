@@ -234,6 +234,22 @@ def extras(torch, dev, sc, flat, plan, mp):
             policy.build_policy(nom, fl, cfg.synthesis, eng, np.random.default_rng(i))
         out["policy_build_ms_e2e"] = 1e3 * (time.perf_counter() - t0) / 3
     plan.set_fluid(flat)
+    # one full replanning cycle at the paper's operating point (nmpc.replan: 10-step
+    # projection, 3 MPPI iterations K=256 over the 67-step tail, nominal, policy; cap 60)
+    from paper_2509_16079_b200 import replan as rp
+    from paper_2509_16079_b200.policy import NominalTrajectory, Policy
+    with np.load(os.path.join(ROOT, "tests", "golden", "nmpc_replan.npz")) as z:
+        gr = {k: z[k] for k in z.files}
+    cfg_r = config.ExperimentConfig()
+    eng_r = rollout.Engine.from_config(cfg_r)
+    pol = Policy(gains=gr["boot_gains"], nominal=NominalTrajectory(gr["boot_states"], gr["boot_inputs"], 0.01))
+    req = rp.ReplanRequest(x=np.asarray(cfg_r.scenario.x0, float), fluid=vpm.FluidState.empty(cfg_r.vpm),
+                           policy=pol, t=0.0, t_proj=10)
+    rp.replan(req, cfg_r, eng_r, np.random.default_rng(1))
+    t0 = time.perf_counter()
+    for i in range(3):
+        rp.replan(req, cfg_r, eng_r, np.random.default_rng(1 + i))
+    out["replan_cycle_ms_e2e"] = 1e3 * (time.perf_counter() - t0) / 3
     # C5: Biot-Savart stress sweep, K=16384 rollouts, attached flow (no shedding, fixed N)
     sweep = {}
     rng = np.random.default_rng(11)

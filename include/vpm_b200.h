@@ -139,6 +139,29 @@ int vpm_plan_batch(vpm_plan *p, const double *d_x0, int x0_stride, const double 
                    int row_end, int T, const double *d_q, const double *d_xperch, int record,
                    const vpm_batch_out *d_out, void *stream);
 
+/* Closed-loop projection (project_forward, nmpc.py:88-103): one rollout of T
+ * Engine.step calls from d_x0 under the feedback policy
+ * u = clip(-K_k (x - tau_k) + xi_k), k = rint((t - t_start)/dt) clamped to
+ * [0, pol_h) (evaluate_policy, policy.py:236-244), t accumulated from t0.  With
+ * write_snapshot the resulting fluid replaces the plan's snapshot on the device
+ * (the MPPI / nominal / policy launches of a replan then fork from it with no host
+ * round trip).  d_status: 0 or 1 + failing step; d_final (7). */
+int vpm_plan_project(vpm_plan *p, const double *d_x0, int T, const double *d_gains,
+                     const double *d_states, const double *d_inputs, int pol_h, double t_start,
+                     double t0, int64_t *d_status, double *d_final, int write_snapshot,
+                     void *stream);
+
+/* Perturbed cloud (perturbed_rollouts, policy.py:66-91) in one launch: row r starts
+ * at x0 + x0_noise[r] * x0_scale and applies clip(u* + u_noise[r] * sigma_u);
+ * trajectories (rows, T+1, 7) recorded. */
+int vpm_plan_cloud(vpm_plan *p, const double *d_x0, const double *d_x0_noise,
+                   const double *d_x0_scale, const double *d_ustar, const double *d_u_noise,
+                   double sigma_u, int rows, int T, int64_t *d_status, double *d_trajs,
+                   void *stream);
+
+/* Copy the plan's (device) snapshot to host buffers (reference _dump_fluid layout). */
+int vpm_plan_download_fluid(vpm_plan *p, vpm_fluid_out *out);
+
 /* MPPI weighted partial sums over rows [0, rows) of this shard
  * (mppi.py:46-59 split for sharding): d_partial (H+2) =
  * {J_min_r, Z_r = sum exp(-(J-J_min_r)/lambda), S_r[H] = sum w u}.  Row r uses

@@ -130,6 +130,11 @@ def lib():
             "vpm_policy_fit_host": (C.c_int, [_D, _D, C.c_int, _D, _D, _I64, C.c_int, C.c_double,
                                               _D, _D, _D, _D]),
             "vpm_tvlqr_host": (C.c_int, [_D, _D, C.c_int, _D, C.c_double, _D, _D]),
+            "vpm_plan_project": (C.c_int, [vp, vp, C.c_int, vp, vp, vp, C.c_int, C.c_double,
+                                           C.c_double, vp, vp, C.c_int, vp]),
+            "vpm_plan_cloud": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_double, C.c_int, C.c_int, vp,
+                                         vp, vp]),
+            "vpm_plan_download_fluid": (C.c_int, [vp, C.POINTER(VpmFluidOut)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -144,7 +149,8 @@ EXPORTED = ("vpm_step", "vpm_rollout", "vpm_batch_rollout", "vpm_batch_rollout_x
             "vpm_plan_batch", "vpm_mppi_partial", "vpm_mppi_combine", "vpm_mppi_iteration",
             "vpm_mppi_optimize_host", "vpm_plan_timing", "vpm_fp32_peak_probe", "vpm_launch_shape",
             "vpm_boundary_inverse", "vpm_policy_fit", "vpm_build_policy_host",
-            "vpm_policy_fit_host", "vpm_tvlqr_host")
+            "vpm_policy_fit_host", "vpm_tvlqr_host", "vpm_plan_project", "vpm_plan_cloud",
+            "vpm_plan_download_fluid")
 
 
 def last_error() -> str:

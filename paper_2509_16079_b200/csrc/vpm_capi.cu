@@ -253,6 +253,8 @@ struct vpm_plan {
   // snapshot
   double *d_wpos = nullptr, *d_wgam = nullptr, *d_ppos = nullptr, *d_pgam = nullptr, *d_ema = nullptr;
   int64_t *d_wage = nullptr;
+  int32_t *d_scal = nullptr;  // device {n_wake, ring_a, ring_b, n_prev}: kernels read these
+  double *d_plev = nullptr;
   int n_wake = 0, ring_a = -1, ring_b = -1, n_prev = 0;
   double prev_lev = 0.0;
   double *d_wbuf = nullptr;
@@ -285,6 +287,8 @@ static Args base_args(const vpm_plan *p) {
   a.n_prev = p->n_prev;
   a.prev_lev = p->prev_lev;
   a.ema = p->d_ema;
+  a.snap_scal = p->d_scal;
+  a.snap_plev = p->d_plev;
   a.integrate = 1;
   a.check_envelope = 1;
   return a;
@@ -346,7 +350,14 @@ vpm_plan *vpm_plan_create(const int64_t *iparams, const double *fparams, int max
             cudaMalloc(&p->d_wage, sizeof(int64_t) * cap4) == cudaSuccess &&
             cudaMalloc(&p->d_ppos, sizeof(double) * 2 * P.nb) == cudaSuccess &&
             cudaMalloc(&p->d_pgam, sizeof(double) * P.nb) == cudaSuccess &&
-            cudaMalloc(&p->d_ema, sizeof(double) * P.nb) == cudaSuccess;
+            cudaMalloc(&p->d_ema, sizeof(double) * P.nb) == cudaSuccess &&
+            cudaMalloc(&p->d_scal, sizeof(int32_t) * 4) == cudaSuccess &&
+            cudaMalloc(&p->d_plev, sizeof(double)) == cudaSuccess;
+  if (ok) {
+    const int32_t empty[4] = {0, -1, -1, 0};
+    ok = cudaMemcpy(p->d_scal, empty, sizeof(empty), cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemset(p->d_plev, 0, sizeof(double)) == cudaSuccess;
+  }
   if (ok) ok = cudaMemcpy(p->d_ainv, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
   if (ok) ok = cudaMemset(p->d_ema, 0, sizeof(double) * P.nb) == cudaSuccess;
   if (!ok) {
@@ -367,6 +378,8 @@ void vpm_plan_destroy(vpm_plan *p) {
   cudaFree(p->d_ppos);
   cudaFree(p->d_pgam);
   cudaFree(p->d_ema);
+  cudaFree(p->d_scal);
+  cudaFree(p->d_plev);
   cudaFree(p->d_wbuf);
   cudaFree(p->hscratch);
   if (p->hstream) cudaStreamDestroy(p->hstream);
@@ -379,6 +392,7 @@ int vpm_plan_set_fluid(vpm_plan *p, const vpm_fluid *f) {
   int rc = check_fluid(f, p->P);
   if (rc) return rc;
   CK(cudaSetDevice(p->device));
+  CK(cudaDeviceSynchronize());  // no launch of any stream may still read the old snapshot
   if (f->n_wake > 0) {
     CK(cudaMemcpy(p->d_wpos, f->wake_pos, sizeof(double) * 2 * f->n_wake, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(p->d_wgam, f->wake_gamma, sizeof(double) * f->n_wake, cudaMemcpyHostToDevice));
@@ -394,6 +408,9 @@ int vpm_plan_set_fluid(vpm_plan *p, const vpm_fluid *f) {
   p->ring_b = f->ring_b;
   p->n_prev = f->n_prev;
   p->prev_lev = f->prev_lev;
+  const int32_t scal[4] = {f->n_wake, f->ring_a, f->ring_b, f->n_prev};
+  CK(cudaMemcpy(p->d_scal, scal, sizeof(scal), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(p->d_plev, &f->prev_lev, sizeof(double), cudaMemcpyHostToDevice));
   return VPM_OK;
 }
 
@@ -429,6 +446,88 @@ int vpm_plan_batch(vpm_plan *p, const double *d_x0, int x0_stride, const double 
   std::lock_guard<std::mutex> lk(p->mu);
   CK(cudaSetDevice(p->device));
   return plan_launch(p, a, a.rows, (cudaStream_t)stream);
+}
+
+int vpm_plan_project(vpm_plan *p, const double *d_x0, int T, const double *d_gains,
+                     const double *d_states, const double *d_inputs, int pol_h, double t_start,
+                     double t0, int64_t *d_status, double *d_final, int write_snapshot,
+                     void *stream) {
+  if (!p) return fail_cfg("null plan");
+  if (T < 0 || pol_h < 1) return fail_cfg("bad projection horizon / policy length");
+  Args a = base_args(p);
+  a.x0 = d_x0;
+  a.T = T;
+  a.rows = 1;
+  a.check_envelope = 0;  // Engine.step semantics (no envelope test, rollout.py:81-86)
+  a.pol_gains = d_gains;
+  a.pol_states = d_states;
+  a.pol_inputs = d_inputs;
+  a.pol_h = pol_h;
+  a.pol_t_start = t_start;
+  a.pol_t0 = t0;
+  a.status = d_status;
+  a.finals = d_final;
+  if (write_snapshot) {
+    // a single CTA reads the snapshot in its prologue and overwrites it in its
+    // epilogue: the projected fluid becomes the plan's snapshot on the device
+    a.need_fluid = 1;
+    a.o_wpos = p->d_wpos;
+    a.o_wgam = p->d_wgam;
+    a.o_wage = p->d_wage;
+    a.o_scal = p->d_scal;
+    a.o_ppos = p->d_ppos;
+    a.o_pgam = p->d_pgam;
+    a.o_plev = p->d_plev;
+    a.o_ema = p->d_ema;
+  }
+  std::lock_guard<std::mutex> lk(p->mu);
+  CK(cudaSetDevice(p->device));
+  return plan_launch(p, a, 1, (cudaStream_t)stream);
+}
+
+int vpm_plan_cloud(vpm_plan *p, const double *d_x0, const double *d_x0_noise,
+                   const double *d_x0_scale, const double *d_ustar, const double *d_u_noise,
+                   double sigma_u, int rows, int T, int64_t *d_status, double *d_trajs,
+                   void *stream) {
+  if (!p) return fail_cfg("null plan");
+  Args a = base_args(p);
+  a.x0 = d_x0;
+  a.x0_noise = d_x0_noise;
+  a.x0_scale = d_x0_scale;
+  a.ustar = d_ustar;
+  a.noise = d_u_noise;
+  a.sigma = sigma_u;
+  a.T = T;
+  a.row_begin = 1;  // MPPI sampling with every row perturbed: row r uses noise row r
+  a.rows = rows;
+  a.record = 1;
+  a.status = d_status;
+  a.trajs = d_trajs;
+  std::lock_guard<std::mutex> lk(p->mu);
+  CK(cudaSetDevice(p->device));
+  return plan_launch(p, a, rows, (cudaStream_t)stream);
+}
+
+int vpm_plan_download_fluid(vpm_plan *p, vpm_fluid_out *out) {
+  if (!p || !out) return fail_cfg("null plan / output");
+  CK(cudaSetDevice(p->device));
+  CK(cudaDeviceSynchronize());
+  const int cap4 = p->P.cap + 4, nb = p->P.nb;
+  CK(cudaMemcpy(out->scalars, p->d_scal, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost));
+  const int n = out->scalars[0];
+  std::memset(out->wake_pos, 0, sizeof(double) * 2 * cap4);
+  std::memset(out->wake_gamma, 0, sizeof(double) * cap4);
+  std::memset(out->wake_age, 0, sizeof(int64_t) * cap4);
+  if (n > 0) {
+    CK(cudaMemcpy(out->wake_pos, p->d_wpos, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out->wake_gamma, p->d_wgam, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out->wake_age, p->d_wage, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+  }
+  CK(cudaMemcpy(out->prev_pos, p->d_ppos, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out->prev_gamma, p->d_pgam, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out->prev_lev, p->d_plev, sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out->ema, p->d_ema, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+  return VPM_OK;
 }
 
 int vpm_mppi_partial(vpm_plan *p, const double *d_cost, int rows, int row_begin,
@@ -852,14 +951,32 @@ int policy_host(vpm_plan *p, const double *nom_x, const double *nom_u, int H, co
   } else {
     CK(cudaGetDevice(&dev));
   }
-  cudaStream_t st;
-  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  // per-thread stream and grow-only scratch: no per-call allocation / stream churn
+  static thread_local cudaStream_t st = nullptr;
+  static thread_local void *buf = nullptr;
+  static thread_local size_t buf_len = 0;
+  static thread_local int buf_dev = -1;
+  if (!st || buf_dev != dev) {
+    if (st) cudaStreamDestroy(st);
+    cudaFree(buf);
+    buf = nullptr;
+    buf_len = 0;
+    st = nullptr;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    buf_dev = dev;
+  }
   const size_t nx = (size_t)K * (H + 1) * 7;
   const size_t need = 16 * 256 + sizeof(double) * ((H + 1) * 7 + H + nx + (size_t)K * H + (size_t)K * 7 +
                                                   14 + H * (15 + 3 + 49 + 7 + 7)) +
                       sizeof(int64_t) * K + 64;
-  void *buf = nullptr;
-  CK(cudaMallocAsync(&buf, need, st));
+  if (buf_len < need) {
+    CK(cudaStreamSynchronize(st));
+    cudaFree(buf);
+    buf = nullptr;
+    buf_len = 0;
+    CK(cudaMalloc(&buf, need));
+    buf_len = need;
+  }
   Carve cv{(char *)buf};
   double *d_nx = cv.take<double>((size_t)(H + 1) * 7), *d_nu = cv.take<double>(H + 1);
   double *d_cx = cv.take<double>(nx + 1), *d_cu = cv.take<double>((size_t)K * H + 1);
@@ -922,10 +1039,7 @@ int policy_host(vpm_plan *p, const double *nom_x, const double *nom_u, int H, co
     if (cloud_x_out && do_fit) CK(cudaMemcpyAsync(cloud_x_out, d_cx, sizeof(double) * nx, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(flag, d_flag, sizeof(flag), cudaMemcpyDeviceToHost, st));
   }
-  cudaFreeAsync(buf, st);
   CK(cudaStreamSynchronize(st));
-  CK(cudaStreamDestroy(st));
-  (void)dev;
   if (rc) return rc;
   if (do_riccati && flag[0]) {
     g_err = "Riccati recursion diverged at step " + std::to_string(flag[0] - 1);

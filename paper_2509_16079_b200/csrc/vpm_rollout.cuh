@@ -95,10 +95,21 @@ struct Args {
   // start state
   const double *x0;
   int x0_stride;
-  // controls: explicit rows, or MPPI sampling from u* and noise
+  // device copies of the snapshot scalars {n_wake, ring_a, ring_b, n_prev} and
+  // prev_lev; when set they override the host values (device-resident snapshots)
+  const int32_t *snap_scal;
+  const double *snap_plev;
+  // per-row start-state perturbation: x0 += x0_noise[row] * x0_scale (policy cloud)
+  const double *x0_noise, *x0_scale;
+  // controls: explicit rows, MPPI sampling from u* and noise, or feedback
   const double *controls;
   const double *ustar, *noise;
   double sigma;
+  // feedback u = clip(-K_k (x - tau_k) + xi_k), k = rint((t - t_start)/dt) clamped
+  // (project_forward, nmpc.py:88-103; evaluate_policy, policy.py:236-244)
+  const double *pol_gains, *pol_states, *pol_inputs;
+  int pol_h;
+  double pol_t_start, pol_t0;
   int T, row_begin, rows;
   int integrate, check_envelope, need_fluid, record;
   // outputs (any may be null)
@@ -132,6 +143,7 @@ struct Ctl {
   int mcnt;     // merge candidates each warp keeps this step
   int fail, status, rc;
   int cur;      // which of the two wake buffers holds the current (raw) wake
+  double tacc;  // feedback mode: simulation time, accumulated like nmpc.py:102
   long long inter;
   unsigned long long shed_mask;
 };
@@ -354,9 +366,17 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
 }
 
 // control of global candidate row g at step t (mppi.py:37-43, :79; _core.pyx:183-187)
-__device__ __forceinline__ double control_at(const Args &a, int row, int t) {
+__device__ __forceinline__ double control_at(const Args &a, int row, int t, const double *x,
+                                             double tacc) {
   double u;
-  if (a.controls) {
+  if (a.pol_gains) {
+    // evaluate_policy (policy.py:236-244): Python round() is round-half-even = rint
+    int k = (int)rint((tacc - a.pol_t_start) / a.P.dt);
+    k = k < 0 ? 0 : (k > a.pol_h - 1 ? a.pol_h - 1 : k);
+    double dot = 0.0;
+    for (int j = 0; j < 7; ++j) dot += a.pol_gains[k * 7 + j] * (x[j] - a.pol_states[k * 7 + j]);
+    u = clampd(-dot + a.pol_inputs[k], -a.P.u_lim, a.P.u_lim);
+  } else if (a.controls) {
     u = a.controls[(size_t)row * a.T + t];
   } else {
     const int g = a.row_begin + row;
@@ -396,15 +416,17 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
   const double dt = P.dt;
 
   // ---- prologue: fork the snapshot into shared memory (_core.pyx:494-526)
-  for (int i = tid; i < a.n_wake; i += NT)
+  const int sn_wake = a.snap_scal ? a.snap_scal[0] : a.n_wake;
+  const int sn_prev = a.snap_scal ? a.snap_scal[3] : a.n_prev;
+  for (int i = tid; i < sn_wake; i += NT)
     wbuf[i] = make_float4((float)a.wpos[2 * i], (float)a.wpos[2 * i + 1],
                           (float)(a.wgam[i] * INV_TWO_PI), __int_as_float((int)a.wage[i]));
-  for (int j = tid; j < a.n_prev; j += NT)
+  for (int j = tid; j < sn_prev; j += NT)
     psrc[j] = make_float4((float)a.ppos[2 * j], (float)a.ppos[2 * j + 1],
                           (float)(a.pgam[j] * INV_TWO_PI), 0.f);
   if (warp == 0) {
     for (int j = lane; j < nb; j += 32) {
-      const bool have = j < a.n_prev;
+      const bool have = j < sn_prev;
       pgp[j] = have ? a.pgam[j] : 0.0;
       pxp[j] = have ? a.ppos[2 * j] : 0.0;
       pzp[j] = have ? a.ppos[2 * j + 1] : 0.0;
@@ -412,20 +434,23 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
     }
     const double *x0 = a.x0 + (size_t)row * a.x0_stride;
     if (lane < 7) {
-      ctl->x[lane] = x0[lane];
-      if (a.record && a.trajs) a.trajs[(size_t)row * (T + 1) * 7 + lane] = x0[lane];
+      double xv = x0[lane];
+      if (a.x0_noise) xv += a.x0_noise[(size_t)row * 7 + lane] * a.x0_scale[lane];
+      ctl->x[lane] = xv;
+      if (a.record && a.trajs) a.trajs[(size_t)row * (T + 1) * 7 + lane] = xv;
     }
     if (lane == 0) {
-      ctl->n_raw = a.n_wake;
-      ctl->n_live = a.n_wake;
+      ctl->n_raw = sn_wake;
+      ctl->n_live = sn_wake;
       ctl->n_holes = 0;
-      ctl->ring_a = a.ring_a;
-      ctl->ring_b = a.ring_b;
-      ctl->n_prev = a.n_prev;
-      ctl->lev_prev = a.prev_lev;
+      ctl->ring_a = a.snap_scal ? a.snap_scal[1] : a.ring_a;
+      ctl->ring_b = a.snap_scal ? a.snap_scal[2] : a.ring_b;
+      ctl->n_prev = sn_prev;
+      ctl->lev_prev = a.snap_plev ? a.snap_plev[0] : a.prev_lev;
+      ctl->tacc = a.pol_t0;
       ctl->lev_cur = 0.0;
       ctl->pending = 0;
-      ctl->mcnt = min(MC, max(0, a.n_wake + 3 - P.cap));
+      ctl->mcnt = min(MC, max(0, sn_wake + 3 - P.cap));
       ctl->fail = 0;
       ctl->status = 0;
       ctl->rc = 0;
@@ -489,6 +514,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           ctl->fwx = Fx; ctl->fwz = Fz; ctl->mw = M;
           ctl->lev_prev = ctl->lev_cur;
           ctl->pending = 0;
+          ctl->tacc += dt;  // nmpc.py:102, t += dt after each step
           if (a.integrate) {
             // elevator + accelerations + forward Euler (_core.pyx:423-461)
             const double th = ctl->x[2], phi = ctl->x[3], u = ctl->u;
@@ -560,7 +586,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           ctl->tz = (rz - fz * s * nb) - P.shed_off * fz;
           ctl->shed = fabs(aoa) > P.crit_aoa;
           ctl->rev = fabs(aoa) > 0.5 * PI;
-          const double u = control_at(a, row, t);
+          const double u = control_at(a, row, t, ctl->x, ctl->tacc);
           ctl->u = clampd(u, -P.u_lim, P.u_lim);
         }
         __syncwarp();

@@ -125,6 +125,38 @@ class DevicePlan:
             float(temperature), _p(q), _p(x_perch), _p(scratch["cost"]), _p(scratch["partial"]),
             _p(scratch["flag"]), 0, _stream(stream)), "mppi_iteration")
 
+    # ---- replan pieces ------------------------------------------------------------------
+    def project(self, x0, T: int, gains, states, inputs, t_start: float, t0: float,
+                write_snapshot: bool = True, stream=None):
+        """Closed-loop projection under a feedback policy (nmpc.py:88-103); returns
+        (status (1,), final (1, 7)) device tensors."""
+        torch = _torch()
+        status = torch.zeros(1, dtype=torch.int64, device=x0.device)
+        final = torch.empty(1, 7, dtype=torch.float64, device=x0.device)
+        check(_lib.lib().vpm_plan_project(
+            self.handle, _p(x0), int(T), _p(gains), _p(states), _p(inputs), int(gains.shape[0]),
+            float(t_start), float(t0), _p(status), _p(final), int(bool(write_snapshot)),
+            _stream(stream)), "plan_project")
+        return status, final
+
+    def cloud(self, x0, x0_noise, x0_scale, ustar, u_noise, sigma_u: float, stream=None):
+        """Perturbed rollout cloud (policy.py:66-91): (status (K,), trajs (K, T+1, 7))."""
+        torch = _torch()
+        K, T = int(u_noise.shape[0]), int(ustar.shape[0])
+        status = torch.empty(K, dtype=torch.int64, device=x0.device)
+        trajs = torch.zeros(K, T + 1, 7, dtype=torch.float64, device=x0.device)
+        check(_lib.lib().vpm_plan_cloud(
+            self.handle, _p(x0), _p(x0_noise), _p(x0_scale), _p(ustar), _p(u_noise), float(sigma_u),
+            K, T, _p(status), _p(trajs), _stream(stream)), "plan_cloud")
+        return status, trajs
+
+    def download_fluid(self):
+        """The plan's current (device) snapshot as the reference's flat 11-tuple."""
+        from ._lib import fluid_out, fluid_tuple
+        fo, bufs = fluid_out(self.cap, self.nb)
+        check(_lib.lib().vpm_plan_download_fluid(self.handle, C.byref(fo)), "download_fluid")
+        return fluid_tuple(bufs)
+
     def timing(self, reset: int = 0):
         """(average rollout-kernel ms, launches) since the last reset; reset=1 starts
         recording CUDA events around every rollout launch, reset=-1 stops."""
@@ -140,6 +172,23 @@ def mppi_combine(partials, temperature: float, ustar, flag=None, stream=None):
     W, ld = int(partials.shape[0]), int(partials.shape[1])
     check(_lib.lib().vpm_mppi_combine(_p(partials), W, ld - 2, float(temperature), _p(ustar),
                                       _p(flag), _stream(stream)), "mppi_combine")
+
+
+def policy_fit(nom_x, nom_u, cloud_x, cloud_u, status, dt: float, q_running, r_running: float,
+               q_final, stream=None):
+    """Device regression + Riccati (policy.py:121-233) on device tensors; returns
+    (a_cont, b_cont, a_disc, b_disc, gains, flag)."""
+    torch = _torch()
+    H, K = int(nom_u.shape[0]), int(cloud_u.shape[0])
+    dev = nom_x.device
+    z = lambda *s: torch.zeros(*s, dtype=torch.float64, device=dev)
+    ac, bc, ad, bd, g = z(H, 3, 5), z(H, 3), z(H, 7, 7), z(H, 7), z(H, 7)
+    flag = torch.zeros(4, dtype=torch.int32, device=dev)
+    check(_lib.lib().vpm_policy_fit(
+        _p(nom_x), _p(nom_u), _p(cloud_x), _p(cloud_u), _p(status), K, H, float(dt), _p(q_running),
+        float(r_running), _p(q_final), _p(ac), _p(bc), _p(ad), _p(bd), _p(g), _p(flag), 1, 1,
+        _stream(stream)), "policy_fit")
+    return ac, bc, ad, bd, g, flag
 
 
 def launch_shape(cap: int, nb: int, rows: int):

@@ -152,5 +152,30 @@ def main():
          dx0=dx0, du=du)
 
 
+def make_replan():
+    """nmpc.bootstrap_policy (rng 0) then one nmpc.replan (rng 1) from x0 at t=0 with
+    the default 10-step projection; default ExperimentConfig (cap 60, horizon 77,
+    K=256).  Written to nmpc_replan.npz."""
+    from perchsim import nmpc
+    cfg = config.ExperimentConfig()
+    eng = rollout.Engine.from_config(cfg)
+    pol = nmpc.bootstrap_policy(cfg, eng, np.random.default_rng(0))
+    fl0 = vpm.FluidState.empty(cfg.vpm)
+    x0 = np.asarray(cfg.scenario.x0, dtype=float)
+    proj = nmpc.project_forward(pol, x0, fl0, 0.0, cfg.scenario.t_proj_steps, eng)
+    req = nmpc.ReplanRequest(x=x0, fluid=fl0, policy=pol, t=0.0, t_proj=cfg.scenario.t_proj_steps)
+    new = nmpc.replan(req, cfg, eng, np.random.default_rng(1))
+    assert proj is not None and new is not None
+    xp, flp, tp = proj
+    save("nmpc_replan.npz", boot_gains=pol.gains, boot_states=pol.nominal.states,
+         boot_inputs=pol.nominal.inputs, proj_x=xp, proj_t=tp, proj_n_wake=flp.n_wake,
+         proj_wake_pos=flp.wake_pos[: flp.n_wake], proj_wake_gamma=flp.wake_gamma[: flp.n_wake],
+         proj_wake_age=flp.wake_age[: flp.n_wake], new_gains=new.gains,
+         new_states=new.nominal.states, new_inputs=new.nominal.inputs, new_t_start=new.t_start)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "replan":
+        make_replan()
+        sys.exit(0)
     main()

@@ -233,6 +233,31 @@ def test_policy_kernels_on_reference_cloud(torch_cuda):
         policy.tvlqr_backward(g["a_discrete"] * 1e200, g["b_discrete"], [1] * 7, 0.01, [1] * 7)
 
 
+def test_replan_on_device_matches_reference(torch_cuda):
+    """nmpc.replan (project 10 closed-loop steps, 3 MPPI iterations K=256 over the
+    67-step tail, nominal rollout, policy) against the reference run with the same
+    bootstrap policy and rng seed (tests/golden/make_golden.py replan)."""
+    from paper_2509_16079_b200 import config, replan, rollout, vpm
+    from paper_2509_16079_b200.policy import NominalTrajectory, Policy
+    g = golden("nmpc_replan.npz")
+    cfg = config.ExperimentConfig()
+    eng = rollout.Engine.from_config(cfg)
+    pol = Policy(gains=g["boot_gains"], nominal=NominalTrajectory(g["boot_states"], g["boot_inputs"], 0.01))
+    x0 = np.asarray(cfg.scenario.x0, dtype=float)
+    fl0 = vpm.FluidState.empty(cfg.vpm)
+    xp, flp, tp = replan.project_forward(pol, x0, fl0, 0.0, 10, eng)
+    assert tp == g["proj_t"] and flp.n_wake == int(g["proj_n_wake"])
+    assert_close(xp, g["proj_x"], what="projected state")
+    np.testing.assert_array_equal(flp.wake_age[: flp.n_wake], g["proj_wake_age"])
+    assert_close(flp.wake_pos[: flp.n_wake], g["proj_wake_pos"], what="projected wake")
+    new = replan.replan(replan.ReplanRequest(x=x0, fluid=fl0, policy=pol, t=0.0, t_proj=10), cfg, eng,
+                        np.random.default_rng(1))
+    assert new is not None and new.t_start == g["new_t_start"]
+    assert_close(new.nominal.inputs, g["new_inputs"], rtol=1e-3, what="replanned u*")
+    assert_close(new.nominal.states, g["new_states"], rtol=1e-3, what="replanned nominal")
+    assert_close(new.gains, g["new_gains"], rtol=5e-2, what="replanned gains")
+
+
 # ------------------------------------------------------------------ full-size properties
 def test_c4_full_batch_properties(torch_cuda, oracle_core):
     """K=4096, H=50, N=512 + ring: deterministic, row-independent (batch ==
