@@ -17,8 +17,6 @@ traffic.  The partial and combine run as device kernels (``vpm_mppi_partial`` /
 
 from __future__ import annotations
 
-import numpy as np
-
 
 def row_range(B: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous block of rows [begin, end) owned by ``rank``; sizes differ by <= 1
@@ -93,9 +91,3 @@ class ShardedMppi:
 
     kernels_per_iteration = 3
 
-
-def interactions_per_iteration(n_live_per_step: np.ndarray, nb: int, n_prev: int) -> int:
-    """Algorithmic regularised Biot-Savart interactions:
-    N(N-1) + n_prev N + nb N (collocation) + nb N' (loads) per rollout-step."""
-    n = np.asarray(n_live_per_step, dtype=np.int64)
-    return int(np.sum(n * (n - 1) + n_prev * n + 2 * nb * n))
