@@ -1077,3 +1077,18 @@ int vpm_tvlqr_host(const double *a_disc, const double *b_disc, int H, const doub
 }
 
 }  // extern "C"
+
+extern "C" int vpm_debug_phase_cycles(unsigned long long *out, int reset) {
+#ifdef VPM_PHASE_TIMING
+  if (out && cudaMemcpyFromSymbol(out, vpm::g_phase, sizeof(vpm::g_phase)) != cudaSuccess) return VPM_ERR_CUDA;
+  if (reset) {
+    static const unsigned long long zero[2][12] = {};
+    if (cudaMemcpyToSymbol(vpm::g_phase, zero, sizeof(zero)) != cudaSuccess) return VPM_ERR_CUDA;
+  }
+  return 24;
+#else
+  (void)out;
+  (void)reset;
+  return VPM_ERR_CONFIG;
+#endif
+}

@@ -63,13 +63,33 @@ constexpr int NB_MAX = 64;     // reference MAXNB (_core.pyx:23)
 constexpr int NT_MAX = 512;    // threads per rollout CTA
 constexpr int NW_MAX = NT_MAX / 32;
 constexpr int MC = 8;          // merge candidates kept per warp
-constexpr int CH = 4;          // source-split targets per chunk
+constexpr int NSEG = 12;       // source segments of the split sweeps (fixed: canonical order)
 constexpr int HOLES_MAX = 16;
 constexpr int WAKE_PAD = 8;    // wake slots beyond cap (reference buffers hold cap+4)
 #ifndef VPM_D_PASS
 #define VPM_D_PASS 1
 #endif
 constexpr int D_PASS = VPM_D_PASS;  // warp 0 runs its control phase after (1) / before (0) its sweep
+
+// Optional per-phase cycle accounting of rollout 0 (threads 0 and 32), for tuning
+// builds only (-DVPM_PHASE_TIMING; read back with vpm_debug_phase_cycles).
+#ifdef VPM_PHASE_TIMING
+__device__ unsigned long long g_phase[2][12];
+#define PHASE_INIT long long ph_last_ = clock64()
+#define PHASE_MARK(i)                                                           \
+  do {                                                                          \
+    if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 32)) {           \
+      const long long now_ = clock64();                                         \
+      g_phase[threadIdx.x >> 5][i] += (unsigned long long)(now_ - ph_last_);    \
+      ph_last_ = now_;                                                          \
+    }                                                                           \
+  } while (0)
+#else
+#define PHASE_INIT
+#define PHASE_MARK(i) \
+  do {                \
+  } while (0)
+#endif
 constexpr double TWO_PI = 6.283185307179586476925286766559;
 constexpr double INV_TWO_PI = 0.15915494309189533576888376337251;
 constexpr double PI = 3.14159265358979323846264338327950288;
@@ -144,6 +164,10 @@ struct Ctl {
   int fail, status, rc;
   int cur;      // which of the two wake buffers holds the current (raw) wake
   double tacc;  // feedback mode: simulation time, accumulated like nmpc.py:102
+  // precomputed by warp 1 while warp 0 runs E of the previous step: the elevator
+  // force of the pending step {Ex, Ez, xe_x, xe_z} and sincos(theta_t)
+  double el[4];
+  double th_sn, th_cs;
   long long inter;
   unsigned long long shed_mask;
 };
@@ -161,7 +185,7 @@ __host__ __device__ inline Layout make_layout(int cap, int nb, int nt) {
   L.capbuf = cap + WAKE_PAD;
   L.nb = nb;
   L.S = nb + 2;
-  L.RS = 2 * nb;                      // floats per source block in the split reductions
+  L.RS = 2 * nb;                      // floats per source segment in the split sweeps
   L.nw = nt / 32;
   L.nblk = (L.capbuf + 31) / 32;      // 32-source blocks
   int off = 2 * L.capbuf * 16;        // double-buffered wake
@@ -177,7 +201,7 @@ __host__ __device__ inline Layout make_layout(int cap, int nb, int nt) {
   off += (13 * L.S + L.nblk) * 8;
   off = align16(off);
   L.off_red = off;
-  off += L.nblk * L.RS * 4;
+  off += NSEG * L.RS * 4;
   off = align16(off);
   L.off_cand = off;
   off += L.nw * MC * 4;
@@ -316,40 +340,32 @@ __device__ __forceinline__ int raw_index(int c, const int *holes, int nh) {
   return r;
 }
 
-// Source-split sweep for a handful of targets tgt[0..nt): warp w takes the
-// 32-source blocks b = w, w+NW, ...; lane l the source 32b + l.  Each block's
-// contribution is reduced with the fixed butterfly and stored per block in
-// red[b * RS + 2k (+1)] = (sum c d'_z, sum c d'_x); consumers add blocks in order.
+// Source-split sweep for a handful of targets tgt[0..nt) (the nb panel or
+// collocation points): the sources are cut into NSEG fixed segments and every
+// (target, segment) pair is one sequential chain on one thread, stored as
+// red[seg * RS + 2k (+1)] = (sum c d'_z, sum c d'_x); consumers add the segments
+// in order.  The cut depends only on n, so the result does not depend on the CTA
+// shape; no cross-lane reductions are needed.
 __device__ __forceinline__ void split_sweep(const float4 *__restrict__ src, int n,
                                             const float2 *tgt, int nt, float rc4, float *red,
-                                            int RS, int warp, int lane, int nw) {
-  const int nblk = (n + 31) >> 5;
-  for (int c0 = 0; c0 < nt; c0 += CH) {
-    float ntx[CH], ntz[CH];
-#pragma unroll
-    for (int k = 0; k < CH; ++k) {
-      const int i = c0 + k < nt ? c0 + k : nt - 1;
-      ntx[k] = -tgt[i].x;
-      ntz[k] = -tgt[i].y;
+                                            int RS, int tid, int nthreads) {
+  const int len = (n + NSEG - 1) / NSEG;
+  for (int task = tid; task < nt * NSEG; task += nthreads) {
+    const int k = task / NSEG, seg = task - k * NSEG;
+    const float ntx = -tgt[k].x, ntz = -tgt[k].y;
+    const int j1 = min(n, (seg + 1) * len);
+    float ax = 0.f, az = 0.f;
+#pragma unroll 4
+    for (int j = seg * len; j < j1; ++j) {
+      const float4 s = src[j];
+      bs_chain(s.x, s.y, s.z, ntx, ntz, rc4, ax, az);
     }
-    for (int b = warp; b < nblk; b += nw) {
-      const int j = 32 * b + lane;
-      float acc[2 * CH];
-#pragma unroll
-      for (int k = 0; k < 2 * CH; ++k) acc[k] = 0.f;
-      if (j < n) {
-        const float4 s = src[j];
-#pragma unroll
-        for (int k = 0; k < CH; ++k) bs_chain(s.x, s.y, s.z, ntx[k], ntz[k], rc4, acc[2 * k], acc[2 * k + 1]);
-      }
-      const float r = warp_reduce8(acc, lane);
-      const int vi = lane >> 2;  // value index: target c0 + vi/2, component vi&1
-      if ((lane & 3) == 0 && c0 + (vi >> 1) < nt) red[b * RS + 2 * c0 + vi] = r;
-    }
+    red[seg * RS + 2 * k] = ax;
+    red[seg * RS + 2 * k + 1] = az;
   }
 }
 
-// wake velocity at split target k from the per-block partials (block order)
+// wake velocity at split target k from the per-segment partials (segment order)
 __device__ __forceinline__ void split_result(const float *red, int RS, int nblk, int k, double &ux,
                                              double &uz) {
   double sx = 0.0, sz = 0.0;
@@ -414,6 +430,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
   const int T = a.T;
   const float rc4 = P.rc4f;
   const double dt = P.dt;
+  PHASE_INIT;
 
   // ---- prologue: fork the snapshot into shared memory (_core.pyx:494-526)
   const int sn_wake = a.snap_scal ? a.snap_scal[0] : a.n_wake;
@@ -473,9 +490,14 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
     const float4 *wsrc = wbuf + cur * L.capbuf;  // raw wake of this iteration (read-only)
     float4 *wk = wbuf + (cur ^ 1) * L.capbuf;    // compacted, advected wake being built
 
-    // ---------------- P1: wake velocity at the panels of step t-1 (its loads)
-    if (pend) split_sweep(wsrc, n_raw, st, nb, rc4, red, RS, warp, lane, NW);
+    // ---------------- P1: wake velocity at the panels of step t-1 (its loads),
+    // source-split over all warps.  (Carrying the 10 panel targets in one warp's
+    // register sweep instead costs that warp a whole extra 32-target slot -- +25%
+    // on the critical path at N=512 -- so the split sweep stays.)
+    if (pend) split_sweep(wsrc, n_raw, st, nb, rc4, red, RS, tid, NT);
+    PHASE_MARK(0);
     __syncthreads();  // B1
+    PHASE_MARK(1);
 
     // P2 runs in two passes: pass D_PASS is warp 0's control work, the other the
     // sweep + advection of every warp.
@@ -483,16 +505,23 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
     // ---------------- P2, control warp: D = loads + integration of step t-1,
     //                  geometry / gates / control of step t
     if (pass == D_PASS && warp == 0) {
+      // The elevator force of the pending step and sincos(theta_t) were computed by
+      // warp 1 during the previous E (they depend only on x_{t-1}, u_{t-1}); lane 29
+      // prefetches the next open-loop control value (a global load).
+      double u_next = 0.0;
+      const bool feedback = a.pol_gains != nullptr;
+      if (conv && lane == 29 && !feedback) u_next = control_at(a, row, t, ctl->x, ctl->tacc);
       if (pend) {
         const double fx = ctl->fx, fz = ctl->fz, nx = ctl->nx, nz = ctl->nz, s = ctl->s;
         const double rx = ctl->x[0], rz = ctl->x[1], vx = ctl->x[4], vz = ctl->x[5], om = ctl->x[6];
+        const double th = ctl->x[2], phi = ctl->x[3], u = ctl->u;
         const int hp = ctl->hp;
         const double xwx = rx - P.l_w * fx, xwz = rz - P.l_w * fz;
         const double dlev = hp ? (ctl->lev_cur - ctl->lev_prev) / dt : 0.0;
-        const int nblk1 = (n_raw + 31) >> 5;
+
         for (int p = lane; p < nb; p += 32) {
           double uxp, uzp;
-          split_result(red, RS, nblk1, p, uxp, uzp);
+          split_result(red, RS, NSEG, p, uxp, uzp);
           double cum = 0.0, cum_prev = 0.0;
           for (int i = 0; i <= p; ++i) { cum += gam[i]; cum_prev += pgp[i]; }
           const double rate = hp ? (cum - cum_prev) / dt + dlev : 0.0;
@@ -507,44 +536,39 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           ema[p] = e;
         }
         __syncwarp();
+        PHASE_MARK(9);
         for (int p = lane; p < nb; p += 32) { pgp[p] = gam[p]; pxp[p] = bx[p]; pzp[p] = bz[p]; }
+        // wing force / moment sums, one component per lane, panel order as _core.pyx:404-406
+        double fc = 0.0;
+        if (lane < 3)
+          for (int p = 0; p < nb; ++p) fc += pf[3 * p + lane];
+        const double Fx = __shfl_sync(0xffffffffu, fc, 0), Fz = __shfl_sync(0xffffffffu, fc, 1);
+        const double M = __shfl_sync(0xffffffffu, fc, 2);
         if (lane == 0) {
-          double Fx = 0.0, Fz = 0.0, M = 0.0;
-          for (int p = 0; p < nb; ++p) { Fx += pf[3 * p]; Fz += pf[3 * p + 1]; M += pf[3 * p + 2]; }
           ctl->fwx = Fx; ctl->fwz = Fz; ctl->mw = M;
           ctl->lev_prev = ctl->lev_cur;
           ctl->pending = 0;
           ctl->tacc += dt;  // nmpc.py:102, t += dt after each step
-          if (a.integrate) {
-            // elevator + accelerations + forward Euler (_core.pyx:423-461)
-            const double th = ctl->x[2], phi = ctl->x[3], u = ctl->u;
-            double se, ce;
-            sincos(th + phi, &se, &ce);
-            const double fex = ce, fez = se, nex = -se, nez = ce;
-            const double xex = rx - P.l * fx - P.l_e * fex, xez = rz - P.l * fz - P.l_e * fez;
-            const double vex = vx - P.l * om * nx - P.l_e * (om + u) * nex;
-            const double vez = vz - P.l * om * nz - P.l_e * (om + u) * nez;
-            const double sp2 = vex * vex + vez * vez;
-            double Ex = 0.0, Ez = 0.0;
-            if (sp2 >= 1e-18) {
-              const double ae = th + phi - atan2(vez, vex);
-              const double cn = 0.5 * P.rho * sp2 * P.s_e * 2.0 * sin(ae);
-              Ex = cn * nex; Ez = cn * nez;
-            }
-            const double ax = (Fx + Ex) / P.m;
-            const double az = (Fz + Ez) / P.m - P.g;
-            const double tq = M + ((xwx - rx) * Fz - (xwz - rz) * Fx) + ((xex - rx) * Ez - (xez - rz) * Ex);
-            const double wd = tq / P.inertia;
-            double xn[7];
-            xn[0] = rx + dt * vx;
-            xn[1] = rz + dt * vz;
-            xn[2] = th + dt * om;
-            xn[3] = clampd(phi + dt * u, -P.phi_lim, P.phi_lim);
-            xn[4] = vx + dt * ax;
-            xn[5] = vz + dt * az;
-            xn[6] = om + dt * wd;
-            bool fin = true;
-            for (int i = 0; i < 7; ++i) { ctl->x[i] = xn[i]; fin = fin && isfinite(xn[i]); }
+        }
+        if (a.integrate) {
+          // accelerations + forward Euler (_core.pyx:439-461), uniform on every lane
+          // (the three divisions are independent and pipeline); the elevator force
+          // comes from warp 1 (ctl->el)
+          const double Ex = ctl->el[0], Ez = ctl->el[1], xex = ctl->el[2], xez = ctl->el[3];
+          const double ax = (Fx + Ex) / P.m;
+          const double az = (Fz + Ez) / P.m - P.g;
+          const double wd =
+              (M + ((xwx - rx) * Fz - (xwz - rz) * Fx) + ((xex - rx) * Ez - (xez - rz) * Ex)) / P.inertia;
+          const double xn[7] = {rx + dt * vx, rz + dt * vz, th + dt * om,
+                                clampd(phi + dt * u, -P.phi_lim, P.phi_lim), vx + dt * ax,
+                                vz + dt * az, om + dt * wd};
+          bool fin = true;
+#pragma unroll
+          for (int i = 0; i < 7; ++i) fin = fin && isfinite(xn[i]);
+#pragma unroll
+          for (int i = 0; i < 7; ++i)
+            if (lane == i) ctl->x[i] = xn[i];
+          if (lane == 0) {
             if (!fin) {
               ctl->fail = 1; ctl->status = t; ctl->rc = 2;
             } else if (a.check_envelope && (fabs(xn[6]) > 300.0 || fabs(xn[4]) > 80.0 || fabs(xn[5]) > 80.0)) {
@@ -553,15 +577,18 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           }
         }
         __syncwarp();
+        PHASE_MARK(10);
         if (a.record && a.trajs && lane < 7 && !ctl->fail)
           a.trajs[((size_t)row * (T + 1) + t) * 7 + lane] = ctl->x[lane];
       }
+      PHASE_MARK(11);
+      if (conv) u_next = __shfl_sync(0xffffffffu, u_next, 29);
       if (conv && !ctl->fail) {
         // chord frame, collocation points, gates of step t (_core.pyx:228-256)
         const double rx = ctl->x[0], rz = ctl->x[1], th = ctl->x[2];
         const double vx = ctl->x[4], vz = ctl->x[5], om = ctl->x[6];
-        double sn, cs;
-        sincos(th, &sn, &cs);
+        double sn = ctl->th_sn, cs = ctl->th_cs;  // sincos(theta_t) from warp 1
+        if (!pend) sincos(th, &sn, &cs);
         const double fx = cs, fz = sn, nx = -sn, nz = cs;
         const double s = P.l_chord / nb;
         for (int i = lane; i <= nb; i += 32) { cx[i] = rx - fx * s * i; cz[i] = rz - fz * s * i; }
@@ -573,10 +600,11 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
         double aoa = 0.0;
         const double vwx = vx - P.l_w * om * nx, vwz = vz - P.l_w * om * nz;
         if (vwx * vwx + vwz * vwz >= 1e-18) {
+          // wrap to (-pi, pi]: the reference's atan2(sin(raw), cos(raw)) equals raw
+          // there up to a few ulp, and aoa only feeds the two gate comparisons
           const double raw = th - atan2(vwz, vwx);
-          double sr, cr;
-          sincos(raw, &sr, &cr);
-          aoa = atan2(sr, cr);
+          aoa = raw - TWO_PI * rint(raw * INV_TWO_PI);
+          if (aoa <= -PI) aoa += TWO_PI;
         }
         if (lane == 0) {
           ctl->fx = fx; ctl->fz = fz; ctl->nx = nx; ctl->nz = nz; ctl->s = s;
@@ -586,7 +614,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           ctl->tz = (rz - fz * s * nb) - P.shed_off * fz;
           ctl->shed = fabs(aoa) > P.crit_aoa;
           ctl->rev = fabs(aoa) > 0.5 * PI;
-          const double u = control_at(a, row, t, ctl->x, ctl->tacc);
+          const double u = feedback ? control_at(a, row, t, ctl->x, ctl->tacc) : u_next;
           ctl->u = clampd(u, -P.u_lim, P.u_lim);
         }
         __syncwarp();
@@ -598,6 +626,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           st[i] = make_float2((float)cx[ri], (float)cz[ri]);
         }
       }
+      PHASE_MARK(2);
     }
     if (pass != D_PASS && conv) {
       // ---------------- P2, all warps: S1 convection sweep of step t, then A
@@ -675,14 +704,51 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
         }
       }
     }
+      PHASE_MARK(3);
     }  // passes
     __syncthreads();  // B2
+    PHASE_MARK(4);
     if (!conv || ctl->fail) break;
 
     // ---------------- S2: wake velocity at the collocation rows of step t
-    split_sweep(wk, n_live, st, nb, rc4, red, RS, warp, lane, NW);
+    split_sweep(wk, n_live, st, nb, rc4, red, RS, tid, NT);
+    PHASE_MARK(5);
     __syncthreads();  // B3
+    PHASE_MARK(6);
 
+    // ---------------- E': warp 1, concurrently with E: the elevator flat-plate force
+    // of the step just solved (it depends only on x_t and u_t, _core.pyx:423-437) and
+    // sincos(theta_{t+1}) for the next geometry -- both off warp 0's critical path
+    if (warp == 1 && lane == 0) {
+      const double rx = ctl->x[0], rz = ctl->x[1], th = ctl->x[2], phi = ctl->x[3];
+      const double vx = ctl->x[4], vz = ctl->x[5], om = ctl->x[6], u = ctl->u;
+      const double fx = ctl->fx, fz = ctl->fz, nx = ctl->nx, nz = ctl->nz;
+      double Ex = 0.0, Ez = 0.0, xex = 0.0, xez = 0.0;
+      if (a.integrate) {
+        double se, ce;
+        sincos(th + phi, &se, &ce);
+        const double fex = ce, fez = se, nex = -se, nez = ce;
+        xex = rx - P.l * fx - P.l_e * fex;
+        xez = rz - P.l * fz - P.l_e * fez;
+        const double vex = vx - P.l * om * nx - P.l_e * (om + u) * nex;
+        const double vez = vz - P.l * om * nz - P.l_e * (om + u) * nez;
+        const double sp2 = vex * vex + vez * vez;
+        if (sp2 >= 1e-18) {
+          const double ae = th + phi - atan2(vez, vex);
+          const double cn = 0.5 * P.rho * sp2 * P.s_e * 2.0 * sin(ae);
+          Ex = cn * nex;
+          Ez = cn * nez;
+        }
+      }
+      ctl->el[0] = Ex;
+      ctl->el[1] = Ez;
+      ctl->el[2] = xex;
+      ctl->el[3] = xez;
+      double sn, cs;
+      sincos(a.integrate ? th + dt * om : th, &sn, &cs);
+      ctl->th_sn = sn;
+      ctl->th_cs = cs;
+    }
     // ---------------- E: solve, shed, merge, ring termination (warp 0)
     if (warp == 0) {
       const int shed = ctl->shed, rev = ctl->rev;
@@ -693,7 +759,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
       const double nx = ctl->nx, nz = ctl->nz;
       for (int i = lane; i < nb; i += 32) {
         double uxw, uzw;
-        split_result(red, RS, nblk2, i, uxw, uzw);
+        split_result(red, RS, NSEG, i, uxw, uzw);
         const int ri = (shed && rev) ? i : i + 1;
         const double px = cx[ri], pz = cz[ri];
         const double svx = vx + om * (-(pz - rz)), svz = vz + om * (px - rx);
@@ -852,7 +918,9 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
         }
       }
     }
+    PHASE_MARK(7);
     __syncthreads();  // B4
+    PHASE_MARK(8);
     if (ctl->fail) break;
   }
   __syncthreads();
