@@ -190,6 +190,14 @@ Shape pick_shape(int cap, int rows) {
     const double ctas = per_sm < 1024.0 / nt ? per_sm : 1024.0 / nt;
     if (ctas * nt >= 768.0) break;
   }
+  // Wave quantisation: with c CTAs resident per SM a launch takes ~ceil(n/c) rounds
+  // of c rollouts per SM.  For 128-thread CTAs, 72 registers (7 CTAs/SM) instead of
+  // 64 (8 CTAs/SM) when that needs fewer rollout-slots in total (4097 rows on 148
+  // SMs: 28 per SM -> 4 x 7 = 28 instead of 4 x 8 = 32).
+  if (best.nt == 128) {
+    const int n_sm = (int)ceil(per_sm);
+    if (n_sm >= 8 && ((n_sm + 6) / 7) * 7 < ((n_sm + 7) / 8) * 8) best.minb = 72;
+  }
   if (const char *m = getenv("VPM_MAXREG")) best.minb = atoi(m);
   return best;
 }
@@ -225,6 +233,8 @@ cudaError_t launch_rollouts(Args a, int grid, cudaStream_t st) {
   const Shape sh = pick_shape(a.P.cap, grid);
   const size_t smem = vpm::make_layout(a.P.cap, a.P.nb, sh.nt).total;
   switch (sh.minb) {
+    case 48: return launch_r<48>(a, grid, sh, smem, st);
+    case 56: return launch_r<56>(a, grid, sh, smem, st);
     case 72: return launch_r<72>(a, grid, sh, smem, st);
     case 80: return launch_r<80>(a, grid, sh, smem, st);
     default: return launch_r<64>(a, grid, sh, smem, st);
