@@ -66,10 +66,18 @@ constexpr int MC = 8;          // merge candidates kept per warp
 constexpr int NSEG = 12;       // source segments of the split sweeps (fixed: canonical order)
 constexpr int HOLES_MAX = 16;
 constexpr int WAKE_PAD = 8;    // wake slots beyond cap (reference buffers hold cap+4)
+#ifndef VPM_SWEEP_UNROLL
+#define VPM_SWEEP_UNROLL 8
+#endif
+#ifndef VPM_SLOT_REV
+#define VPM_SLOT_REV 1
+#endif
 #ifndef VPM_D_PASS
 #define VPM_D_PASS 1
 #endif
+constexpr int SWEEP_UNROLL = VPM_SWEEP_UNROLL;  // sources per sweep-loop trip
 constexpr int D_PASS = VPM_D_PASS;  // warp 0 runs its control phase after (1) / before (0) its sweep
+constexpr bool SLOT_REV = VPM_SLOT_REV;  // last warp takes the odd 32-particle block, not warp 0
 
 // Optional per-phase cycle accounting of rollout 0 (threads 0 and 32), for tuning
 // builds only (-DVPM_PHASE_TIMING; read back with vpm_debug_phase_cycles).
@@ -249,7 +257,7 @@ __device__ __forceinline__ void sweep_tile(const float4 *__restrict__ src, int n
   }
   const float2 rc = make_float2(rc4, rc4);
   float ox = (K & 1) ? ax[K - 1] : 0.f, oz = (K & 1) ? az[K - 1] : 0.f;
-#pragma unroll 2
+#pragma unroll SWEEP_UNROLL
   for (int j = 0; j < n; ++j) {
     const float4 s = src[j];
     const float2 sx = make_float2(s.x, s.x), sz = make_float2(s.y, s.y), sg = make_float2(s.z, s.z);
@@ -635,7 +643,8 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
       //  holds the reference's failure-time wake).  Slot k of warp w holds the
       //  particles c = 32 (NW k + w) + lane; warp 0 takes its slots after D.
       const int kmax = R;
-      auto slot_base = [&](int k) { return 32 * (NW * k + warp); };
+      const int wslot = SLOT_REV ? NW - 1 - warp : warp;
+      auto slot_base = [&](int k) { return 32 * (NW * k + wslot); };
       float ux[R], uz[R];
       {
         float ntx[R], ntz[R], bx_[R], bz_[R];
