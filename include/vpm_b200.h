@@ -241,6 +241,14 @@ int vpm_boundary_inverse(const int64_t *iparams, const double *fparams, double *
  * memory bytes. */
 int vpm_launch_shape(int cap, int nb, int rows, int *threads, int *targets, int *smem_bytes);
 
+/* Host buffers: velocity induced by n point vortices (pos (n,2), gamma (n)) at m
+ * target points (targets (m,2)) -> out (m,2), FP64 on the device.  kernel 0 is the
+ * regularised kernel with core radius r_core, 1 the singular kernel (a coincident
+ * source contributes 0).  Replaces vpm.induced_velocity_at (vpm.py:105-128), the
+ * NMPC pressure sensor's flow model (nmpc.py:71-85). */
+int vpm_induced_velocity_host(const double *pos, const double *gamma, int n, const double *targets,
+                              int m, double r_core, int kernel, double *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -122,6 +122,7 @@ def lib():
             "vpm_fp32_peak_probe": (C.c_double, [C.c_int, C.c_int]),
             "vpm_launch_shape": (C.c_int, [C.c_int, C.c_int, C.c_int, _I32, _I32, _I32]),
             "vpm_boundary_inverse": (C.c_int, [_I64, _D, _D]),
+            "vpm_induced_velocity_host": (C.c_int, [_D, _D, C.c_int, _D, C.c_int, C.c_double, C.c_int, _D]),
             "vpm_policy_fit": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_double, vp,
                                          C.c_double, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int,
                                          vp]),
@@ -150,7 +151,7 @@ EXPORTED = ("vpm_step", "vpm_rollout", "vpm_batch_rollout", "vpm_batch_rollout_x
             "vpm_mppi_optimize_host", "vpm_plan_timing", "vpm_fp32_peak_probe", "vpm_launch_shape",
             "vpm_boundary_inverse", "vpm_policy_fit", "vpm_build_policy_host",
             "vpm_policy_fit_host", "vpm_tvlqr_host", "vpm_plan_project", "vpm_plan_cloud",
-            "vpm_plan_download_fluid")
+            "vpm_plan_download_fluid", "vpm_induced_velocity_host")
 
 
 def last_error() -> str:

@@ -1086,6 +1086,32 @@ int vpm_tvlqr_host(const double *a_disc, const double *b_disc, int H, const doub
                      nullptr, nullptr, 0, 1);
 }
 
+int vpm_induced_velocity_host(const double *pos, const double *gamma, int n, const double *targets,
+                              int m, double r_core, int kernel, double *out) {
+  if (n < 0 || m < 0) return fail_cfg("negative point count");
+  if (kernel != 0 && kernel != 1) return fail_cfg("kernel must be 0 (regularised) or 1 (singular)");
+  if (m == 0) return VPM_OK;
+  HostCtx &h = g_host;
+  if (!h.st) CK(cudaStreamCreateWithFlags(&h.st, cudaStreamNonBlocking));
+  void *sc = host_scratch(256 * 4 + sizeof(double) * (3 * (size_t)n + 4 * (size_t)m + 4));
+  if (!sc) return fail_cfg("device scratch allocation failed");
+  Carve cv{(char *)sc};
+  double *d_pos = cv.take<double>(2 * (size_t)n + 1), *d_gam = cv.take<double>((size_t)n + 1);
+  double *d_tg = cv.take<double>(2 * (size_t)m), *d_out = cv.take<double>(2 * (size_t)m);
+  if (n > 0) {
+    CK(cudaMemcpyAsync(d_pos, pos, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, h.st));
+    CK(cudaMemcpyAsync(d_gam, gamma, sizeof(double) * n, cudaMemcpyHostToDevice, h.st));
+  }
+  CK(cudaMemcpyAsync(d_tg, targets, sizeof(double) * 2 * m, cudaMemcpyHostToDevice, h.st));
+  const double rc2 = r_core * r_core;
+  vpm::induced_velocity_kernel<<<(m + 3) / 4, 128, 0, h.st>>>(d_pos, d_gam, n, d_tg, m, rc2 * rc2, kernel,
+                                                              d_out);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d_out, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost, h.st));
+  CK(cudaStreamSynchronize(h.st));
+  return VPM_OK;
+}
+
 }  // extern "C"
 
 extern "C" int vpm_debug_phase_cycles(unsigned long long *out, int reset) {

@@ -1308,6 +1308,36 @@ __global__ void __launch_bounds__(512) policy_kernel(const PolicyArgs p) {
 // Pipe throughput probes, 8 independent chains per thread.
 //   MODE 0: FFMA (2 flop / lane / op)   MODE 1: FFMA2 packed f32x2 (4 flop / lane / op)
 //   MODE 2: MUFU.RSQ (1 op / lane)
+// Velocity induced by n point vortices at m target points, FP64 (vpm.py:93-128):
+// kernel 0 regularised  Gamma [dz, -dx] / (2 pi sqrt(r^4 + rc^4)),  kernel 1 singular
+// Gamma [dz, -dx] / (2 pi r^2) with a coincident source contributing 0.  One warp
+// per target: lane-strided partial sums in source order, then a fixed butterfly,
+// so the result does not depend on the launch.  Used by the NMPC pressure sensor.
+__global__ void induced_velocity_kernel(const double *__restrict__ pos, const double *__restrict__ gam,
+                                        int n, const double *__restrict__ tg, int m, double rc4,
+                                        int singular, double *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= m) return;
+  const double tx = tg[2 * i], tz = tg[2 * i + 1];
+  double ux = 0.0, uz = 0.0;
+  for (int j = lane; j < n; j += 32) {
+    const double dx = tx - pos[2 * j], dz = tz - pos[2 * j + 1];
+    const double r2 = dx * dx + dz * dz;
+    double c;
+    if (singular) c = r2 == 0.0 ? 0.0 : gam[j] / (TWO_PI * r2);
+    else c = gam[j] / (TWO_PI * sqrt(r2 * r2 + rc4));
+    ux += c * dz;
+    uz -= c * dx;
+  }
+  ux = warp_sum_d(ux);
+  uz = warp_sum_d(uz);
+  if (lane == 0) {
+    out[2 * i] = ux;
+    out[2 * i + 1] = uz;
+  }
+}
+
 template <int MODE>
 __global__ void fp32_probe_kernel(float *out, int iters, float a, float b) {
   float s = 0.f;

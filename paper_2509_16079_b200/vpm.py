@@ -5,7 +5,9 @@ vpm.py:144-234, ``VortexParticle``, ``RingDisturbance`` / ``inject_ring`` /
 ``ring_circulation_for_speed`` vpm.py:486-536): these are value-semantics host
 snapshots that the planner forks onto the device.  All stepping physics of the
 reference module (kernels, boundary solve, convection, shedding, merging, loads)
-runs in the CUDA library, not here.
+runs in the CUDA library, not here; ``induced_velocity`` / ``induced_velocity_at``
+(vpm.py:93-128, the flow model of the NMPC pressure sensor) call the library's
+FP64 device kernel.
 """
 
 from __future__ import annotations
@@ -18,6 +20,39 @@ import numpy as np
 from .config import VpmConfig
 
 TWO_PI = 2.0 * math.pi
+KERNEL_REGULARIZED = "regularized"
+KERNEL_SINGULAR = "singular"
+_KERNEL_ID = {KERNEL_REGULARIZED: 0, KERNEL_SINGULAR: 1}
+
+
+def induced_velocity_at(targets, positions, gammas, kernel: str = KERNEL_REGULARIZED,
+                        r_core: float = 0.0) -> np.ndarray:
+    """Velocity induced at each of the (m, 2) ``targets`` by point vortices at
+    ``positions`` with circulations ``gammas`` (vpm.py:105-128), computed in FP64 on
+    the device (``vpm_induced_velocity_host``).  Unknown kernels raise ValueError."""
+    from . import _lib
+
+    if kernel not in _KERNEL_ID:
+        raise ValueError(f"unknown kernel {kernel!r}")
+    tg = np.ascontiguousarray(np.atleast_2d(np.asarray(targets, dtype=np.float64)))
+    out = np.zeros_like(tg)
+    n = 0 if gammas is None else len(gammas)
+    if n == 0 or len(tg) == 0:
+        return out
+    pos = np.ascontiguousarray(np.asarray(positions, dtype=np.float64).reshape(n, 2))
+    gam = np.ascontiguousarray(np.asarray(gammas, dtype=np.float64))
+    D = _lib._D
+    _lib.check(_lib.lib().vpm_induced_velocity_host(_lib.ptr(pos, D), _lib.ptr(gam, D), n, _lib.ptr(tg, D),
+                                                     len(tg), float(r_core), _KERNEL_ID[kernel],
+                                                     _lib.ptr(out, D)), "induced_velocity")
+    return out
+
+
+def induced_velocity(positions, gammas, target, kernel: str = KERNEL_REGULARIZED,
+                     r_core: float = 0.0) -> np.ndarray:
+    """Summed velocity of many vortices at one target point (vpm.py:93-102)."""
+    return induced_velocity_at(np.asarray(target, dtype=float).reshape(1, 2), positions, gammas,
+                               kernel, r_core)[0]
 
 
 @dataclass

@@ -79,6 +79,57 @@ __global__ void sweep_kernel(float *out, int n, int reps, float rc4) {
   if (s == 1.2345f) out[blockIdx.x] = s;
 }
 
+// Symmetric-pair tile: lane holds 2*KP "i" targets (packed pairs) and one rotating
+// "j" particle whose data (x, z, g) and packed accumulator travel one lane per step
+// (7 SHFL per step); every (i, j) pair is evaluated once and updates both sides.
+template <int KP>
+__global__ void sym_kernel(float *out, int reps, float rc4) {
+  const int lane = threadIdx.x & 31;
+  float2 px[KP], pz[KP], pg[KP], ax[KP], az[KP];
+#pragma unroll
+  for (int p = 0; p < KP; ++p) {
+    px[p] = make_float2(0.013f * (lane + p), 0.017f * p);
+    pz[p] = make_float2(0.011f * p, 0.019f * (lane & 3));
+    pg[p] = make_float2(1e-3f * (p + 1), -1e-3f * (lane & 1));
+    ax[p] = az[p] = make_float2(0.f, 0.f);
+  }
+  float jx = 0.021f * lane, jz = -0.01f * lane, jg = 2e-3f;
+  float2 bx = make_float2(0.f, 0.f), bz = make_float2(0.f, 0.f);
+  const float2 rc = make_float2(rc4, rc4);
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+      const float2 sx = make_float2(jx, jx), sz = make_float2(jz, jz), sg = make_float2(jg, jg);
+#pragma unroll
+      for (int p = 0; p < KP; ++p) {
+        const float2 dx = __fadd2_rn(sx, px[p]);
+        const float2 dz = __fadd2_rn(sz, pz[p]);
+        const float2 r2 = __ffma2_rn(dx, dx, __fmul2_rn(dz, dz));
+        const float2 q = __ffma2_rn(r2, r2, rc);
+        const float2 rs = make_float2(rsq(q.x), rsq(q.y));
+        const float2 ci = __fmul2_rn(sg, rs);
+        ax[p] = __ffma2_rn(ci, dz, ax[p]);
+        az[p] = __ffma2_rn(ci, dx, az[p]);
+        const float2 cj = __fmul2_rn(pg[p], rs);
+        bx = __ffma2_rn(cj, dz, bx);
+        bz = __ffma2_rn(cj, dx, bz);
+      }
+      const int src = (lane + 1) & 31;
+      jx = __shfl_sync(0xffffffffu, jx, src);
+      jz = __shfl_sync(0xffffffffu, jz, src);
+      jg = __shfl_sync(0xffffffffu, jg, src);
+      bx.x = __shfl_sync(0xffffffffu, bx.x, src);
+      bx.y = __shfl_sync(0xffffffffu, bx.y, src);
+      bz.x = __shfl_sync(0xffffffffu, bz.x, src);
+      bz.y = __shfl_sync(0xffffffffu, bz.y, src);
+    }
+  }
+  float s = jx + bx.x + bx.y + bz.x + bz.y;
+#pragma unroll
+  for (int p = 0; p < KP; ++p) s += ax[p].x + ax[p].y + az[p].x + az[p].y;
+  if (s == 1.2345f) out[blockIdx.x] = s;
+}
+
 static int g_sms, g_clk_khz;
 
 template <typename F>
@@ -121,22 +172,29 @@ static void run_sweep(float *out, int n, int threads, int ctas_per_sm) {
          threads, ctas_per_sm, inter / clk / g_sms);
 }
 
+template <int KP>
+static void run_sym(float *out, int threads, int ctas_per_sm) {
+  const int reps = 200;
+  const int grid = g_sms * ctas_per_sm * 4;
+  float ms = time_ms([&] { sym_kernel<KP><<<grid, threads>>>(out, reps, 1e-4f); });
+  // directed interactions: 2 per (i, j) pair; 2*KP pairs per lane per step
+  const double inter = (double)grid * threads * reps * 32 * 2 * KP * 2;
+  const double clk = ms * 1e-3 * g_clk_khz * 1e3;
+  printf("{\"probe\":\"sym\",\"pairs\":%d,\"threads\":%d,\"ctas\":%d,\"directed_per_clk_sm\":%.2f}\n", KP, threads,
+         ctas_per_sm, inter / clk / g_sms);
+}
+
 int main() {
   cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0);
   cudaDeviceGetAttribute(&g_clk_khz, cudaDevAttrClockRate, 0);
   float *out;
   cudaMalloc(&out, 1 << 24);
-  run_mix<4, 8, 2>(out, 7, 128);
-  for (int cps : {7}) {
-    run_sweep<2, 1>(out, 512, 128, cps);
-    run_sweep<2, 2>(out, 512, 128, cps);
-    run_sweep<2, 4>(out, 512, 128, cps);
-    run_sweep<2, 8>(out, 512, 128, cps);
-    run_sweep<3, 1>(out, 512, 128, cps);
-    run_sweep<3, 2>(out, 512, 128, cps);
-    run_sweep<3, 4>(out, 512, 128, cps);
-    run_sweep<4, 1>(out, 512, 128, cps);
-    run_sweep<4, 4>(out, 512, 128, cps);
+  run_sweep<2, 8>(out, 512, 128, 7);
+  for (int c : {4, 7}) {
+    run_sym<1>(out, 128, c);
+    run_sym<2>(out, 128, c);
+    run_sym<3>(out, 128, c);
+    run_sym<4>(out, 128, c);
   }
   printf("{\"sms\":%d,\"clk_mhz\":%d}\n", g_sms, g_clk_khz / 1000);
   return 0;
