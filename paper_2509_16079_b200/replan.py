@@ -63,63 +63,103 @@ def project_forward(policy: Policy, x, fluid: FluidState, t: float, t_proj: int,
     return final[0].cpu().numpy(), engine._rebuild(flat), _projection_time(t, t_proj, engine.cfg.dt)
 
 
+def _staging(plan, n: int):
+    """Grow-only pinned host buffer on the plan (async H2D of the cycle's draws)."""
+    import torch
+    buf = getattr(plan, "_replan_pinned", None)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(max(n, 1), dtype=torch.float64, pin_memory=True)
+        plan._replan_pinned = buf
+    return buf[:n]
+
+
 def replan(req: ReplanRequest, cfg: ExperimentConfig, engine: Engine,
            rng: np.random.Generator) -> Policy | None:
-    """Project, re-optimise, rebuild the policy (nmpc.py:106-134); None when rejected."""
+    """Project, re-optimise, rebuild the policy (nmpc.py:106-134); None when rejected.
+
+    The whole cycle is queued on one stream with a single host synchronisation at
+    the end: projection -> MPPI iterations -> one launch of the nominal rollout
+    (row 0, zero perturbation: bitwise the reference's ``rollout(x_proj, u*)``)
+    together with the 64-rollout cloud (rows 1..64) -> regression + Riccati.  All
+    random numbers of the success path are drawn up front, in the reference's order
+    (iteration noises, then the cloud's dx0 and du), while the projection runs.
+    The reference stops drawing at its first failure (nmpc.py:118-134); when the
+    cycle turns out to have failed at such a point, the generator is rewound and
+    exactly the draws the reference made before failing are replayed, so the
+    caller's generator ends in the reference's state either way.
+    """
     torch, plan, dev, f64 = _dev(engine)
     dt = engine.cfg.dt
     lim = engine.params.u_limit
-    plan.set_fluid(req.fluid)
     old = req.policy.nominal
-    # 1. closed-loop projection; its wake becomes the plan's snapshot on the device
-    status, xdev = plan.project(f64(req.x), int(req.t_proj), f64(req.policy.gains),
-                                f64(old.states), f64(old.inputs), old.t_start, float(req.t),
-                                write_snapshot=True)
-    if int(status.item()) != 0:
-        return None
     t_new = _projection_time(float(req.t), int(req.t_proj), dt)
     k0 = int(round((t_new - old.t_start) / dt))
     tail = old.inputs[k0:]
     if len(tail) == 0:
-        return None
+        return None  # nothing to re-plan; the reference draws nothing on this path either
+    plan.set_fluid(req.fluid)
+    # 1. closed-loop projection; its wake becomes the plan's snapshot on the device
+    pstat, xdev = plan.project(f64(req.x), int(req.t_proj), f64(req.policy.gains), f64(old.states),
+                               f64(old.inputs), old.t_start, float(req.t), write_snapshot=True)
     x0 = xdev[0]
-    # 2. MPPI iterations (mppi.py:62-84) on the projected state and wake
-    mc = cfg.mppi
-    u = f64(np.clip(np.asarray(tail, dtype=float), -lim, lim))
-    H, K, iters = u.shape[0], int(mc.batch), int(mc.iterations)
-    if H and iters and K:
+    mc, sc = cfg.mppi, cfg.synthesis
+    H, K, iters, k = len(tail), int(mc.batch), int(mc.iterations), int(sc.n_samples)
+    run_mppi = bool(H and iters and K)
+    # 2. the success path's draws (host, overlapping the projection on the device)
+    saved = rng.bit_generator.state
+    noise = rng.normal(0.0, 1.0, (iters, K, H)) if run_mppi else np.zeros((0, K, H))
+    dx0 = rng.normal(0.0, 1.0, (k, 7))
+    du = rng.normal(0.0, 1.0, (k, H))
+    n_noise, n_cloud = noise.size, (k + 1) * 7 + (k + 1) * H
+    host = _staging(plan, n_noise + n_cloud + H)
+    hv = host.numpy()
+    hv[:n_noise] = noise.ravel()
+    cx = hv[n_noise:n_noise + (k + 1) * 7].reshape(k + 1, 7)
+    cu = hv[n_noise + (k + 1) * 7:n_noise + n_cloud].reshape(k + 1, H)
+    cx[0], cx[1:] = 0.0, dx0  # row 0: the nominal, unperturbed
+    cu[0], cu[1:] = 0.0, du
+    hv[n_noise + n_cloud:] = np.clip(np.asarray(tail, dtype=float), -lim, lim)
+    dbuf = host.to(dev, non_blocking=True)
+    d_noise = dbuf[:n_noise].view(iters, K, H) if run_mppi else None
+    d_cx = dbuf[n_noise:n_noise + (k + 1) * 7].view(k + 1, 7)
+    d_cu = dbuf[n_noise + (k + 1) * 7:n_noise + n_cloud].view(k + 1, H)
+    u = dbuf[n_noise + n_cloud:].clone()
+    # 3. MPPI iterations (mppi.py:62-84), one failure flag per iteration
+    flags = torch.zeros(max(iters, 1), dtype=torch.int32, device=dev)
+    if run_mppi:
         scratch = {"cost": torch.empty(K + 1, dtype=torch.float64, device=dev),
-                   "partial": torch.empty(H + 2, dtype=torch.float64, device=dev),
-                   "flag": torch.zeros(1, dtype=torch.int32, device=dev)}
+                   "partial": torch.empty(H + 2, dtype=torch.float64, device=dev)}
         q, xp = f64(mc.q_terminal), f64(mc.x_perch)
-        for _ in range(iters):  # one draw per iteration, as mppi.py:42 (stops on failure)
-            noise = f64(rng.normal(0.0, 1.0, (K, H)))
-            plan.mppi_iteration(x0, u, noise, mc.input_stdev, K + 1, mc.temperature, q, xp, scratch)
-            if int(scratch["flag"].item()) != 0:
-                return None  # mppi.optimize raised ValueError
-    # 3. nominal rollout of the new plan (nmpc.py:127)
-    nomout = plan.batch(x0, H, controls=u.view(1, H), rows=1, record=True)
-    if int(nomout["status"].item()) != 0:
+        for i in range(iters):
+            scratch["flag"] = flags[i:i + 1]
+            plan.mppi_iteration(x0, u, d_noise[i], mc.input_stdev, K + 1, mc.temperature, q, xp, scratch)
+    # 4. nominal (row 0) + perturbed cloud (rows 1..k) in one launch (policy.py:66-91)
+    cstat, ctraj = plan.cloud(x0, d_cx, f64(sc.state_stdev), u, d_cu, sc.input_stdev)
+    traj = ctraj[0]
+    cu_dev = torch.clamp(u.view(1, H) + d_cu[1:] * sc.input_stdev, -lim, lim)
+    # 5. regression + Riccati around the nominal (policy.py:247-266)
+    _, _, _, _, gains, fflag = policy_fit(traj, u, ctraj[1:], cu_dev, cstat[1:], dt, f64(sc.q_running),
+                                          sc.r_running, f64(sc.q_final))
+    # 6. the one synchronisation: every decision the reference makes, in its order
+    ints = torch.cat([pstat.view(1), flags.to(torch.int64), cstat, fflag[:1].to(torch.int64)]).cpu().numpy()
+    if ints[0] != 0:
+        rng.bit_generator.state = saved  # projection failed before any draw
         return None
-    traj = nomout["trajs"][0]
-    # 4. policy synthesis around it (policy.py:247-266): cloud, regression, Riccati
-    sc = cfg.synthesis
-    k = int(sc.n_samples)
-    dx0 = f64(rng.normal(0.0, 1.0, (k, 7)))
-    du = f64(rng.normal(0.0, 1.0, (k, H)))
-    cstat, ctraj = plan.cloud(traj[0].contiguous(), dx0, f64(sc.state_stdev), u, du, sc.input_stdev)
-    survivors = int((cstat == 0).sum().item())
-    if survivors < 6:
-        return None  # RankDeficientData
-    cu = torch.clamp(u.view(1, H) + du * sc.input_stdev, -lim, lim)
-    _, _, _, _, gains, flag = policy_fit(traj.contiguous(), u, ctraj, cu, cstat, dt, f64(sc.q_running),
-                                         sc.r_running, f64(sc.q_final))
-    if int(flag[0].item()) != 0:
-        return None  # FloatingPointError
-    nominal = NominalTrajectory(states=traj.cpu().numpy(), inputs=u.cpu().numpy(), dt=dt,
-                                t_start=t_new)
-    return Policy(gains=gains.cpu().numpy(), nominal=nominal,
-                  q_final=np.asarray(sc.q_final, dtype=float))
+    for i in range(iters if run_mppi else 0):
+        if ints[1 + i] != 0:  # mppi.optimize raised ValueError after drawing i + 1 noises
+            rng.bit_generator.state = saved
+            rng.normal(0.0, 1.0, (i + 1, K, H))
+            return None
+    st = ints[1 + max(iters, 1):1 + max(iters, 1) + k + 1]
+    if st[0] != 0:  # nominal rollout failed: the reference drew the MPPI noise only
+        rng.bit_generator.state = saved
+        if run_mppi:
+            rng.normal(0.0, 1.0, (iters, K, H))
+        return None
+    if int((st[1:] == 0).sum()) < 6 or ints[-1] != 0:
+        return None  # RankDeficientData / FloatingPointError after all draws
+    nominal = NominalTrajectory(states=traj.cpu().numpy(), inputs=u.cpu().numpy(), dt=dt, t_start=t_new)
+    return Policy(gains=gains.cpu().numpy(), nominal=nominal, q_final=np.asarray(sc.q_final, dtype=float))
 
 
 def bootstrap_policy(cfg: ExperimentConfig, engine: Engine, rng: np.random.Generator) -> Policy:

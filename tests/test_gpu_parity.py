@@ -258,6 +258,42 @@ def test_replan_on_device_matches_reference(torch_cuda):
     assert_close(new.gains, g["new_gains"], rtol=5e-2, what="replanned gains")
 
 
+def test_replan_leaves_the_generator_where_the_reference_does(torch_cuda):
+    """The replan draws every random number up front; the caller's generator must
+    still end exactly where the reference's would (nmpc.py:118-134): after a
+    success, iters x (K, H) MPPI noises then the cloud's (64, 7) and (64, H); after a
+    failed projection, untouched."""
+    from paper_2509_16079_b200 import config, replan, rollout, vpm
+    from paper_2509_16079_b200.policy import NominalTrajectory, Policy
+    g = golden("nmpc_replan.npz")
+    cfg = config.ExperimentConfig()
+    eng = rollout.Engine.from_config(cfg)
+    pol = Policy(gains=g["boot_gains"], nominal=NominalTrajectory(g["boot_states"], g["boot_inputs"], 0.01))
+    x0 = np.asarray(cfg.scenario.x0, dtype=float)
+    fl0 = vpm.FluidState.empty(cfg.vpm)
+    rng, twin = np.random.default_rng(11), np.random.default_rng(11)
+    new = replan.replan(replan.ReplanRequest(x=x0, fluid=fl0, policy=pol, t=0.0, t_proj=10), cfg, eng, rng)
+    assert new is not None
+    H = new.nominal.horizon
+    for _ in range(cfg.mppi.iterations):
+        twin.normal(0.0, 1.0, (cfg.mppi.batch, H))
+    twin.normal(0.0, 1.0, (cfg.synthesis.n_samples, 7))
+    twin.normal(0.0, 1.0, (cfg.synthesis.n_samples, H))
+    assert rng.bit_generator.state == twin.bit_generator.state
+    # the nominal of the fused nominal+cloud launch is the plain rollout of u*
+    rc, traj, _ = eng.rollout(new.nominal.states[0], new.nominal.inputs, replan.project_forward(
+        pol, x0, fl0, 0.0, 10, eng)[1], record=True)
+    assert rc == 0
+    np.testing.assert_array_equal(traj, new.nominal.states)
+    # a projection that leaves the envelope rejects the replan without drawing
+    bad = x0.copy()
+    bad[6] = 400.0
+    before = rng.bit_generator.state
+    assert replan.replan(replan.ReplanRequest(x=bad, fluid=fl0, policy=pol, t=0.0, t_proj=10), cfg, eng,
+                         rng) is None
+    assert rng.bit_generator.state == before
+
+
 # ------------------------------------------------------------------ full-size properties
 def test_c4_full_batch_properties(torch_cuda, oracle_core):
     """K=4096, H=50, N=512 + ring: deterministic, row-independent (batch ==
