@@ -80,9 +80,10 @@ def replan(req: ReplanRequest, cfg: ExperimentConfig, engine: Engine,
     The whole cycle is queued on one stream with a single host synchronisation at
     the end: projection -> MPPI iterations -> one launch of the nominal rollout
     (row 0, zero perturbation: bitwise the reference's ``rollout(x_proj, u*)``)
-    together with the 64-rollout cloud (rows 1..64) -> regression + Riccati.  All
-    random numbers of the success path are drawn up front, in the reference's order
-    (iteration noises, then the cloud's dx0 and du), while the projection runs.
+    together with the 64-rollout cloud (rows 1..64) -> regression + Riccati.  The
+    random numbers of the success path are drawn in the reference's order
+    (iteration noises, then the cloud's dx0 and du), each while the device runs
+    the previous launch.
     The reference stops drawing at its first failure (nmpc.py:118-134); when the
     cycle turns out to have failed at such a point, the generator is rewound and
     exactly the draws the reference made before failing are replayed, so the
@@ -105,34 +106,37 @@ def replan(req: ReplanRequest, cfg: ExperimentConfig, engine: Engine,
     mc, sc = cfg.mppi, cfg.synthesis
     H, K, iters, k = len(tail), int(mc.batch), int(mc.iterations), int(sc.n_samples)
     run_mppi = bool(H and iters and K)
-    # 2. the success path's draws (host, overlapping the projection on the device)
+    # 2./3. the success path's draws and the MPPI iterations (mppi.py:62-84),
+    # pipelined: each iteration's noise is drawn on the host and copied while the
+    # device runs the previous launch; one failure flag per iteration
     saved = rng.bit_generator.state
-    noise = rng.normal(0.0, 1.0, (iters, K, H)) if run_mppi else np.zeros((0, K, H))
-    dx0 = rng.normal(0.0, 1.0, (k, 7))
-    du = rng.normal(0.0, 1.0, (k, H))
-    n_noise, n_cloud = noise.size, (k + 1) * 7 + (k + 1) * H
-    host = _staging(plan, n_noise + n_cloud + H)
+    n_it = K * H if run_mppi else 0
+    n_cloud = (k + 1) * 7 + (k + 1) * H
+    host = _staging(plan, H + iters * n_it + n_cloud)
     hv = host.numpy()
-    hv[:n_noise] = noise.ravel()
-    cx = hv[n_noise:n_noise + (k + 1) * 7].reshape(k + 1, 7)
-    cu = hv[n_noise + (k + 1) * 7:n_noise + n_cloud].reshape(k + 1, H)
-    cx[0], cx[1:] = 0.0, dx0  # row 0: the nominal, unperturbed
-    cu[0], cu[1:] = 0.0, du
-    hv[n_noise + n_cloud:] = np.clip(np.asarray(tail, dtype=float), -lim, lim)
-    dbuf = host.to(dev, non_blocking=True)
-    d_noise = dbuf[:n_noise].view(iters, K, H) if run_mppi else None
-    d_cx = dbuf[n_noise:n_noise + (k + 1) * 7].view(k + 1, 7)
-    d_cu = dbuf[n_noise + (k + 1) * 7:n_noise + n_cloud].view(k + 1, H)
-    u = dbuf[n_noise + n_cloud:].clone()
-    # 3. MPPI iterations (mppi.py:62-84), one failure flag per iteration
+    hv[:H] = np.clip(np.asarray(tail, dtype=float), -lim, lim)
+    u = host[:H].to(dev, non_blocking=True)
     flags = torch.zeros(max(iters, 1), dtype=torch.int32, device=dev)
     if run_mppi:
         scratch = {"cost": torch.empty(K + 1, dtype=torch.float64, device=dev),
                    "partial": torch.empty(H + 2, dtype=torch.float64, device=dev)}
         q, xp = f64(mc.q_terminal), f64(mc.x_perch)
         for i in range(iters):
+            lo = H + i * n_it
+            hv[lo:lo + n_it] = rng.normal(0.0, 1.0, (K, H)).ravel()
+            d_noise = host[lo:lo + n_it].to(dev, non_blocking=True).view(K, H)
             scratch["flag"] = flags[i:i + 1]
-            plan.mppi_iteration(x0, u, d_noise[i], mc.input_stdev, K + 1, mc.temperature, q, xp, scratch)
+            plan.mppi_iteration(x0, u, d_noise, mc.input_stdev, K + 1, mc.temperature, q, xp, scratch)
+    lo = H + iters * n_it
+    dx0 = rng.normal(0.0, 1.0, (k, 7))
+    du = rng.normal(0.0, 1.0, (k, H))
+    cx = hv[lo:lo + (k + 1) * 7].reshape(k + 1, 7)
+    cu = hv[lo + (k + 1) * 7:lo + n_cloud].reshape(k + 1, H)
+    cx[0], cx[1:] = 0.0, dx0  # row 0: the nominal, unperturbed
+    cu[0], cu[1:] = 0.0, du
+    dcl = host[lo:lo + n_cloud].to(dev, non_blocking=True)
+    d_cx = dcl[:(k + 1) * 7].view(k + 1, 7)
+    d_cu = dcl[(k + 1) * 7:].view(k + 1, H)
     # 4. nominal (row 0) + perturbed cloud (rows 1..k) in one launch (policy.py:66-91)
     cstat, ctraj = plan.cloud(x0, d_cx, f64(sc.state_stdev), u, d_cu, sc.input_stdev)
     traj = ctraj[0]
