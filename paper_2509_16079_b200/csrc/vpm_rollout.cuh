@@ -83,19 +83,29 @@ constexpr bool SLOT_REV = VPM_SLOT_REV;  // last warp takes the odd 32-particle 
 // builds only (-DVPM_PHASE_TIMING; read back with vpm_debug_phase_cycles).
 #ifdef VPM_PHASE_TIMING
 __device__ unsigned long long g_phase[2][12];
-#define PHASE_INIT long long ph_last_ = clock64()
-#define PHASE_MARK(i)                                                           \
-  do {                                                                          \
-    if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 32)) {           \
-      const long long now_ = clock64();                                         \
-      g_phase[threadIdx.x >> 5][i] += (unsigned long long)(now_ - ph_last_);    \
-      ph_last_ = now_;                                                          \
-    }                                                                           \
+// cycles accumulate in registers (a global read-modify-write per mark would sit on
+// the critical path); PHASE_FLUSH writes them once after the step loop
+#define PHASE_INIT                  \
+  long long ph_last_ = clock64();   \
+  unsigned long long ph_acc_[12] = {}
+#define PHASE_MARK(i)                                                   \
+  do {                                                                  \
+    const long long now_ = clock64();                                   \
+    ph_acc_[i] += (unsigned long long)(now_ - ph_last_);                \
+    ph_last_ = now_;                                                    \
+  } while (0)
+#define PHASE_FLUSH                                                                 \
+  do {                                                                              \
+    if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 32))                 \
+      for (int i_ = 0; i_ < 12; ++i_) g_phase[threadIdx.x >> 5][i_] += ph_acc_[i_]; \
   } while (0)
 #else
 #define PHASE_INIT
 #define PHASE_MARK(i) \
   do {                \
+  } while (0)
+#define PHASE_FLUSH \
+  do {              \
   } while (0)
 #endif
 constexpr double TWO_PI = 6.283185307179586476925286766559;
@@ -665,8 +675,10 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           bx_[k] = 0.f;
           bz_[k] = 0.f;
         }
-        sweep_dispatch<R>(kw, wsrc, n_raw, ntx, ntz, ux, uz, rc4);
-        sweep_dispatch<R>(kw, psrc, n_prev, ntx, ntz, bx_, bz_, rc4);
+        if (kw > 0) {  // a warp without live targets skips the calls (and their spills)
+          sweep_dispatch<R>(kw, wsrc, n_raw, ntx, ntz, ux, uz, rc4);
+          sweep_dispatch<R>(kw, psrc, n_prev, ntx, ntz, bx_, bz_, rc4);
+        }
 #pragma unroll
         for (int k = 0; k < R; ++k) {
           ux[k] = -ux[k] - bx_[k];  // u_x = -(wake chain) - (bound-row chain)
@@ -933,6 +945,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
     if (ctl->fail) break;
   }
   __syncthreads();
+  PHASE_FLUSH;
 
   // ---- epilogue: outputs
   if (tid == 0) {
