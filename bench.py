@@ -402,6 +402,7 @@ def run_ours(args):
     nt, r, smem = launch_shape(CAP, 10, mp.end - mp.begin)
     peak_meas = fp32_peak_gflops() / 1e3
     peak = max(peak_meas, FP32_SPEC_TFLOPS)
+    mix_ceiling = max(fp32_peak_gflops(4096, 3) for _ in range(2)) / 1e3  # FP32+MUFU mix probe
     flops_per_launch = 12.0 * inter_all / max(world, 1)
     achieved = flops_per_launch / (kern_ms_max * 1e-3) / 1e12 if kern_ms_max > 0 else None
     line = {
@@ -419,7 +420,12 @@ def run_ours(args):
                      "flop_per_launch": flops_per_launch,
                      "kernel_ms": kern_ms_max,
                      "peak_source": f"max(FFMA probe {peak_meas:.1f}, spec 148x128x2x1.965GHz "
-                                    f"{FP32_SPEC_TFLOPS:.1f}) TFLOP/s; MEASURED_PEAKS.json has no FP32 entry"},
+                                    f"{FP32_SPEC_TFLOPS:.1f}) TFLOP/s; MEASURED_PEAKS.json has no FP32 entry",
+                     "formulation_ceiling": {
+                         "value": mix_ceiling, "unit": "TFLOP/s", "frac_of_peak": mix_ceiling / peak,
+                         "achieved_frac_of_ceiling": (achieved / mix_ceiling) if achieved else None,
+                         "source": "probe of the direct kernel's instruction mix (8 FP32 lane-ops + "
+                                   "1 MUFU.RSQ per interaction, independent chains, no loads)"}},
         "gpu_launches": ShardedMppi.kernels_per_iteration * args.steps,
         "clocks": clk.summary(),
     }

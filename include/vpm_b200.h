@@ -228,7 +228,9 @@ int vpm_tvlqr_host(const double *a_disc, const double *b_disc, int H, const doub
 int vpm_plan_timing(vpm_plan *p, int reset, double *avg_ms, int64_t *launches);
 
 /* Pipe throughput microbenchmark on the current device: mode 0 FFMA (GFLOP/s),
- * 1 packed FFMA2 (GFLOP/s), 2 MUFU.RSQ (G ops/s). */
+ * 1 packed FFMA2 (GFLOP/s), 2 MUFU.RSQ (G ops/s), 3 the direct Biot-Savart
+ * instruction mix (8 FP32 lane-ops + 1 MUFU.RSQ per interaction) in algorithmic
+ * GFLOP/s at 12 flop per interaction -- the formulation's pipe ceiling. */
 double vpm_fp32_peak_probe(int iters, int mode);
 
 /* Host-only: the inverses of the three pose-invariant boundary systems the solve

@@ -163,9 +163,9 @@ int device_sms() {
 }
 
 // Launch shape.  A rollout CTA has NT threads; each holds R register target slots
-// (slot k of warp w = particles 32 (NW k + w) .. +31) covering cap + 4 (the
+// (slot k of warp w = particles 32 (NW k + NW-1-w) .. +31) covering cap + 4 (the
 // largest wake a snapshot may hold), so every particle is a register target.
-// Warp 0 runs the FP64 loads / dynamics / geometry phase before its slots.  NT is
+// Warp 0 runs the FP64 loads / dynamics / geometry phase after its slots.  NT is
 // the smallest of 64..512 that still puts >= 24 warps on every SM given how many
 // rollouts each SM receives (4097 rollouts on one GPU -> 128 x 5, 512 per GPU at
 // 8 GPUs -> 256 x 3).  Results do not depend on the shape (canonical reduction
@@ -677,7 +677,8 @@ double vpm_fp32_peak_probe(int iters, int mode) {
   float *d = nullptr;
   if (cudaMalloc(&d, blocks * sizeof(float)) != cudaSuccess) return -1.0;
   auto run = [&](int it) {
-    if (mode == 1) vpm::fp32_probe_kernel<1><<<blocks, threads>>>(d, it, 0.9999f, 1e-4f);
+    if (mode == 3) vpm::fp32_probe_kernel<3><<<blocks, threads>>>(d, it, 0.9999f, 1e-4f);
+    else if (mode == 1) vpm::fp32_probe_kernel<1><<<blocks, threads>>>(d, it, 0.9999f, 1e-4f);
     else if (mode == 2) vpm::fp32_probe_kernel<2><<<blocks, threads>>>(d, it, 0.9999f, 1e-4f);
     else vpm::fp32_probe_kernel<0><<<blocks, threads>>>(d, it, 0.9999f, 1e-4f);
   };
@@ -694,8 +695,10 @@ double vpm_fp32_peak_probe(int iters, int mode) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(d);
-  // GFLOP/s for FFMA (2/lane-op) and FFMA2 (4/lane-op); G ops/s for MUFU
-  const double per = mode == 1 ? 4.0 : (mode == 2 ? 1.0 : 2.0);
+  // GFLOP/s for FFMA (2/lane-op) and FFMA2 (4/lane-op); G ops/s for MUFU; mode 3:
+  // algorithmic Biot-Savart GFLOP/s of the mix (4 chains x 2 interactions per
+  // thread-iteration, 12 flop each)
+  const double per = mode == 1 ? 4.0 : (mode == 2 ? 1.0 : (mode == 3 ? 12.0 : 2.0));
   const double work = per * 8.0 * (double)iters * blocks * threads;
   return ms > 0.f ? work / (ms * 1e-3) / 1e9 : -1.0;
 }

@@ -1354,7 +1354,29 @@ __global__ void induced_velocity_kernel(const double *__restrict__ pos, const do
 template <int MODE>
 __global__ void fp32_probe_kernel(float *out, int iters, float a, float b) {
   float s = 0.f;
-  if constexpr (MODE == 1) {
+  if constexpr (MODE == 3) {
+    // the direct Biot-Savart mix: per packed pair of interactions 8 packed FP32 ops
+    // and 2 MUFU.RSQ, 4 independent chains (the formulation's pipe ceiling)
+    float2 v[4], w[4];
+    const float2 A = make_float2(a, a);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] = make_float2(1.f + threadIdx.x * 1e-3f + i, 2.f + i);
+      w[i] = make_float2(b, 0.5f * b);
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float2 t = v[i];
+#pragma unroll
+        for (int f = 0; f < 7; ++f) t = __ffma2_rn(t, A, w[i]);
+        t = make_float2(rsqrt_mufu(t.x), rsqrt_mufu(t.y));
+        v[i] = __ffma2_rn(t, A, v[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s += v[i].x + v[i].y;
+  } else if constexpr (MODE == 1) {
     float2 v[8];
     const float2 A = make_float2(a, a), Bv = make_float2(b, b);
 #pragma unroll
