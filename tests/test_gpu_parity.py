@@ -391,3 +391,47 @@ def test_envelope_blowup_status(torch_cuda, oracle_core):
     d = oracle_core.batch_rollout_diag(x0, ctrl, *fl.flat(), eng.iparams, eng.fparams)
     np.testing.assert_array_equal(res.status, d["status"])
     assert (res.status > 0).all()
+
+
+def test_concurrent_callers_get_independent_results(torch_cuda):
+    """The stepping module is called from two threads in threaded NMPC mode (plant
+    loop + replanning worker, nmpc.py:219-222; SURVEY 8b 'Threading'): concurrent
+    Engine.step / Engine.batch calls from several threads must return exactly what
+    the same calls return one at a time."""
+    import threading
+
+    from paper_2509_16079_b200 import config, rollout, vpm
+    cfg = config.ExperimentConfig()
+    eng = rollout.Engine.from_config(cfg)
+    x0 = np.array([0.0, 0.0, 0.3, 0.0, 7.0, 0.0, 0.0])
+
+    def stepping(seed):
+        fl, x = vpm.FluidState.empty(cfg.vpm), x0.copy()
+        us = np.random.default_rng(seed).uniform(-15, 15, 40)
+        out = []
+        for u in us:
+            ok, x, fl, _ = eng.step(x, u, fl)
+            out.append(x.copy())
+        return np.array(out), fl.wake_pos.copy()
+
+    def batching(seed):
+        u = np.random.default_rng(seed).uniform(-15, 15, (64, 30))
+        res = eng.batch(rollout.RolloutRequest(x0=x0, fluid=vpm.FluidState.empty(cfg.vpm), controls=u))
+        return res.status.copy(), res.finals.copy()
+
+    jobs = [(stepping, s) for s in range(3)] + [(batching, s) for s in range(3)]
+    serial = [fn(s) for fn, s in jobs]
+    got = [None] * len(jobs)
+
+    def run(i):
+        for _ in range(3):
+            got[i] = jobs[i][0](jobs[i][1])
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(jobs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for a, b in zip(serial, got):
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
