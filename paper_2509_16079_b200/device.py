@@ -66,6 +66,16 @@ class DevicePlan:
             _lib._lib.vpm_plan_destroy(h)
             self.handle = None
 
+    def staging(self, n: int):
+        """Grow-only pinned host buffer of n float64 (async H2D of per-call draws).
+        Callers synchronise before reusing it."""
+        torch = _torch()
+        buf = getattr(self, "_pinned", None)
+        if buf is None or buf.numel() < n:
+            buf = torch.empty(max(int(n), 1), dtype=torch.float64, pin_memory=True)
+            self._pinned = buf
+        return buf[:n]
+
     def set_fluid(self, fluid) -> None:
         flat = fluid.flat() if hasattr(fluid, "flat") else tuple(fluid)
         f, keep = fluid_struct(*flat)

@@ -2,12 +2,12 @@
 
 ``optimize`` keeps the reference signature and random-number consumption: it
 draws exactly what the reference draws from ``rng`` (one ``normal(0, 1, (K, H))``
-block per iteration -- drawn here as one ``(iters, K, H)`` block, which numpy's
-Generator fills identically) and hands everything to one C-ABI call,
-``vpm_mppi_optimize_host``.  On the device each iteration is: one persistent
-rollout kernel over the K+1 candidates (row 0 = incumbent, rows 1..K =
-clip(u* + sigma * noise)) with the terminal cost fused into its epilogue, one
-softmax-partial kernel and one combine kernel.
+block per iteration, each drawn while the device runs the previous iteration).
+On the device each iteration is: one persistent rollout kernel over the K+1
+candidates (row 0 = incumbent, rows 1..K = clip(u* + sigma * noise)) with the
+terminal cost fused into its epilogue, one softmax-partial kernel and one combine
+kernel (the same launches as the host-buffer C entry point
+``vpm_mppi_optimize_host``, which takes all noise up front).
 
 ``terminal_cost``, ``terminal_cost_batch``, ``sample_controls`` and
 ``mppi_update`` are small host utilities on host arrays, kept for API parity;
@@ -18,8 +18,6 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import _lib
-from ._lib import _D, as_f64, check, ptr
 from .config import MppiConfig
 from .rollout import Engine
 from .vpm import FluidState
@@ -58,23 +56,50 @@ def mppi_update(controls, costs, temperature: float) -> np.ndarray:
 
 def optimize(x0, fluid: FluidState, warm_start, cfg: MppiConfig, engine: Engine,
              rng: np.random.Generator, iterations: int | None = None) -> np.ndarray:
-    """Iterated sample / rollout / reweight on the GPU; returns the final u*."""
+    """Iterated sample / rollout / reweight on the GPU; returns the final u*.
+
+    Iteration i's noise is drawn on the host (exactly the reference's
+    ``normal(0, 1, (K, H))`` call) while the device runs iteration i-1; the host
+    synchronises once, at the end.  If an iteration finds every candidate failed,
+    the reference raises after drawing that iteration's noise and no more: the
+    generator is rewound and those draws replayed before ``ValueError`` is raised,
+    so the caller's generator ends where the reference leaves it."""
     u_lim = engine.params.u_limit
     u = np.clip(np.asarray(warm_start, dtype=float).copy(), -u_lim, u_lim)
     iters = cfg.iterations if iterations is None else iterations
     H, K = len(u), int(cfg.batch)
     if H == 0 or iters == 0 or K == 0:
         return u
-    noise = as_f64(rng.normal(0.0, 1.0, (iters, K, H)))
+    import torch
     plan = engine_plan(engine)
+    dev = torch.device("cuda", plan.device)
     plan.set_fluid(fluid)
-    q = as_f64(cfg.q_terminal)
-    xp = as_f64(cfg.x_perch)
-    x0a = as_f64(x0)
-    check(_lib.lib().vpm_mppi_optimize_host(
-        plan.handle, ptr(x0a, _D), ptr(u, _D), ptr(noise, _D), iters, K, H,
-        float(cfg.input_stdev), float(cfg.temperature), ptr(q, _D), ptr(xp, _D)), "mppi.optimize")
-    return u
+    n_it = K * H
+    host = plan.staging(H + 7 + 14 + iters * n_it)
+    hv = host.numpy()
+    hv[:H] = u
+    hv[H:H + 7] = np.asarray(x0, dtype=float)
+    hv[H + 7:H + 14] = np.asarray(cfg.q_terminal, dtype=float)
+    hv[H + 14:H + 21] = np.asarray(cfg.x_perch, dtype=float)
+    head = host[:H + 21].to(dev, non_blocking=True)
+    u_dev, x0d, q, xp = head[:H].clone(), head[H:H + 7], head[H + 7:H + 14], head[H + 14:H + 21]
+    flags = torch.zeros(iters, dtype=torch.int32, device=dev)
+    scratch = {"cost": torch.empty(K + 1, dtype=torch.float64, device=dev),
+               "partial": torch.empty(H + 2, dtype=torch.float64, device=dev)}
+    saved = rng.bit_generator.state
+    for i in range(iters):
+        lo = H + 21 + i * n_it
+        hv[lo:lo + n_it] = rng.normal(0.0, 1.0, (K, H)).ravel()
+        d_noise = host[lo:lo + n_it].to(dev, non_blocking=True).view(K, H)
+        scratch["flag"] = flags[i:i + 1]
+        plan.mppi_iteration(x0d, u_dev, d_noise, cfg.input_stdev, K + 1, cfg.temperature, q, xp, scratch)
+    out = torch.cat([u_dev, flags.to(torch.float64)]).cpu().numpy()
+    bad = np.nonzero(out[H:] != 0)[0]
+    if bad.size:
+        rng.bit_generator.state = saved
+        rng.normal(0.0, 1.0, (int(bad[0]) + 1, K, H))
+        raise ValueError("all sampled rollouts failed (infinite cost)")
+    return out[:H].copy()
 
 
 def engine_plan(engine: Engine):

@@ -63,16 +63,6 @@ def project_forward(policy: Policy, x, fluid: FluidState, t: float, t_proj: int,
     return final[0].cpu().numpy(), engine._rebuild(flat), _projection_time(t, t_proj, engine.cfg.dt)
 
 
-def _staging(plan, n: int):
-    """Grow-only pinned host buffer on the plan (async H2D of the cycle's draws)."""
-    import torch
-    buf = getattr(plan, "_replan_pinned", None)
-    if buf is None or buf.numel() < n:
-        buf = torch.empty(max(n, 1), dtype=torch.float64, pin_memory=True)
-        plan._replan_pinned = buf
-    return buf[:n]
-
-
 def replan(req: ReplanRequest, cfg: ExperimentConfig, engine: Engine,
            rng: np.random.Generator) -> Policy | None:
     """Project, re-optimise, rebuild the policy (nmpc.py:106-134); None when rejected.
@@ -112,7 +102,7 @@ def replan(req: ReplanRequest, cfg: ExperimentConfig, engine: Engine,
     saved = rng.bit_generator.state
     n_it = K * H if run_mppi else 0
     n_cloud = (k + 1) * 7 + (k + 1) * H
-    host = _staging(plan, H + iters * n_it + n_cloud)
+    host = plan.staging(H + iters * n_it + n_cloud)
     hv = host.numpy()
     hv[:H] = np.clip(np.asarray(tail, dtype=float), -lim, lim)
     u = host[:H].to(dev, non_blocking=True)

@@ -435,3 +435,32 @@ def test_concurrent_callers_get_independent_results(torch_cuda):
     for a, b in zip(serial, got):
         for x, y in zip(a, b):
             np.testing.assert_array_equal(x, y)
+
+
+def test_optimize_pipeline_equals_host_entry_and_rewinds_on_failure(torch_cuda):
+    """mppi.optimize (per-iteration draws overlapped with the device) returns bitwise
+    what the all-up-front C entry point vpm_mppi_optimize_host returns, and when
+    every candidate fails it raises ValueError leaving the generator exactly where
+    the reference leaves it (iteration 0's draw only)."""
+    from paper_2509_16079_b200 import _lib, config, mppi
+    from paper_2509_16079_b200._lib import _D, as_f64, ptr
+    sc = golden("scenario_C2.npz")
+    eng = engine_for(sc["iparams"], sc["fparams"])
+    mcfg = config.MppiConfig(batch=256, iterations=3, horizon=50)
+    fl = fluid_from(sc, 60)
+    u_pipe = mppi.optimize(sc["x0"], fl, sc["warm"], mcfg, eng, np.random.default_rng(4))
+    noise = as_f64(np.random.default_rng(4).normal(0.0, 1.0, (3, 256, 50)))
+    plan = mppi.engine_plan(eng)
+    plan.set_fluid(fl)
+    u_host = np.clip(np.asarray(sc["warm"], float), -15, 15).copy()
+    q, xp, x0 = as_f64(mcfg.q_terminal), as_f64(mcfg.x_perch), as_f64(sc["x0"])
+    assert _lib.lib().vpm_mppi_optimize_host(plan.handle, ptr(x0, _D), ptr(u_host, _D), ptr(noise, _D), 3,
+                                             256, 50, 2.0, 0.05, ptr(q, _D), ptr(xp, _D)) == 0
+    np.testing.assert_array_equal(u_pipe, u_host)
+    bad = np.asarray(sc["x0"], float).copy()
+    bad[6] = 400.0  # leaves the envelope on the first step: every candidate fails
+    rng, twin = np.random.default_rng(8), np.random.default_rng(8)
+    with pytest.raises(ValueError):
+        mppi.optimize(bad, fl, sc["warm"], mcfg, eng, rng)
+    twin.normal(0.0, 1.0, (256, 50))
+    assert rng.bit_generator.state == twin.bit_generator.state
