@@ -78,6 +78,12 @@ int unpack(const int64_t *ip, const double *fp, Phys *P) {
   P->eta = fp[FP_ETA];
   const double r = P->r_core;
   P->rc4f = (float)(r * r * r * r);
+  P->inv_dt = 1.0 / P->dt;
+  P->inv_m = 1.0 / P->m;
+  P->inv_inertia = 1.0 / P->inertia;
+  P->s_pan = P->l_chord / P->nb;
+  P->inv_s = 1.0 / P->s_pan;
+  P->cos_crit = P->crit_aoa >= vpm::PI ? -2.0 : std::cos(P->crit_aoa);
   return VPM_OK;
 }
 

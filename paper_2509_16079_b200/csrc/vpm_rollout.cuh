@@ -116,6 +116,9 @@ struct Phys {
   int nb, cap;
   double r_core, k_diss, shed_off, crit_aoa, rho, dt, m, inertia, g, l, l_w, l_e, l_chord, s_e,
       phi_lim, u_lim, lev_gain, eta;
+  // derived on the host: reciprocals of the constant divisors of the per-step
+  // chain, panel length, cos(critical aoa) (-2 when the gate can never open)
+  double inv_dt, inv_m, inv_inertia, s_pan, inv_s, cos_crit;
   float rc4f;
 };
 
@@ -405,7 +408,7 @@ __device__ __forceinline__ double control_at(const Args &a, int row, int t, cons
   double u;
   if (a.pol_gains) {
     // evaluate_policy (policy.py:236-244): Python round() is round-half-even = rint
-    int k = (int)rint((tacc - a.pol_t_start) / a.P.dt);
+    int k = (int)rint((tacc - a.pol_t_start) * a.P.inv_dt);
     k = k < 0 ? 0 : (k > a.pol_h - 1 ? a.pol_h - 1 : k);
     double dot = 0.0;
     for (int j = 0; j < 7; ++j) dot += a.pol_gains[k * 7 + j] * (x[j] - a.pol_states[k * 7 + j]);
@@ -535,18 +538,18 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
         const double th = ctl->x[2], phi = ctl->x[3], u = ctl->u;
         const int hp = ctl->hp;
         const double xwx = rx - P.l_w * fx, xwz = rz - P.l_w * fz;
-        const double dlev = hp ? (ctl->lev_cur - ctl->lev_prev) / dt : 0.0;
+        const double dlev = hp ? (ctl->lev_cur - ctl->lev_prev) * P.inv_dt : 0.0;
 
         for (int p = lane; p < nb; p += 32) {
           double uxp, uzp;
           split_result(red, RS, NSEG, p, uxp, uzp);
           double cum = 0.0, cum_prev = 0.0;
           for (int i = 0; i <= p; ++i) { cum += gam[i]; cum_prev += pgp[i]; }
-          const double rate = hp ? (cum - cum_prev) / dt + dlev : 0.0;
+          const double rate = hp ? (cum - cum_prev) * P.inv_dt + dlev : 0.0;
           const double e = P.eta * rate + (1.0 - P.eta) * (hp ? ema[p] : 0.0);
           const double svx = vx + om * (-(bz[p] - rz)), svz = vz + om * (bx[p] - rx);
           const double beta = (uxp - svx) * fx + (uzp - svz) * fz;
-          const double dp = P.rho * (beta * gam[p] / s + e);
+          const double dp = P.rho * (beta * gam[p] * P.inv_s + e);
           const double pfx = dp * s * nx, pfz = dp * s * nz;
           pf[3 * p] = pfx;
           pf[3 * p + 1] = pfz;
@@ -573,10 +576,10 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           // (the three divisions are independent and pipeline); the elevator force
           // comes from warp 1 (ctl->el)
           const double Ex = ctl->el[0], Ez = ctl->el[1], xex = ctl->el[2], xez = ctl->el[3];
-          const double ax = (Fx + Ex) / P.m;
-          const double az = (Fz + Ez) / P.m - P.g;
+          const double ax = (Fx + Ex) * P.inv_m;
+          const double az = (Fz + Ez) * P.inv_m - P.g;
           const double wd =
-              (M + ((xwx - rx) * Fz - (xwz - rz) * Fx) + ((xex - rx) * Ez - (xez - rz) * Ex)) / P.inertia;
+              (M + ((xwx - rx) * Fz - (xwz - rz) * Fx) + ((xex - rx) * Ez - (xez - rz) * Ex)) * P.inv_inertia;
           const double xn[7] = {rx + dt * vx, rz + dt * vz, th + dt * om,
                                 clampd(phi + dt * u, -P.phi_lim, P.phi_lim), vx + dt * ax,
                                 vz + dt * az, om + dt * wd};
@@ -608,21 +611,24 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
         double sn = ctl->th_sn, cs = ctl->th_cs;  // sincos(theta_t) from warp 1
         if (!pend) sincos(th, &sn, &cs);
         const double fx = cs, fz = sn, nx = -sn, nz = cs;
-        const double s = P.l_chord / nb;
+        const double s = P.s_pan;
         for (int i = lane; i <= nb; i += 32) { cx[i] = rx - fx * s * i; cz[i] = rz - fz * s * i; }
         for (int j = lane; j < nb; j += 32) {
           const double c0x = rx - fx * s * j, c0z = rz - fz * s * j;
           bx[j] = c0x - 0.5 * s * fx;
           bz[j] = c0z - 0.5 * s * fz;
         }
-        double aoa = 0.0;
+        // gates on the effective angle of attack aoa = wrap(theta - atan2(vw)) of
+        // _core.pyx:247-256, tested without the angle: cos(aoa) = f.vw / |vw|, so
+        // |aoa| > crit  <=>  f.vw < cos(crit) |vw|  and  |aoa| > pi/2  <=>  f.vw < 0
+        // (|aoa| in [0, pi]; a vanishing relative wind gives aoa = 0, no gate)
+        bool g_shed = false, g_rev = false;
         const double vwx = vx - P.l_w * om * nx, vwz = vz - P.l_w * om * nz;
-        if (vwx * vwx + vwz * vwz >= 1e-18) {
-          // wrap to (-pi, pi]: the reference's atan2(sin(raw), cos(raw)) equals raw
-          // there up to a few ulp, and aoa only feeds the two gate comparisons
-          const double raw = th - atan2(vwz, vwx);
-          aoa = raw - TWO_PI * rint(raw * INV_TWO_PI);
-          if (aoa <= -PI) aoa += TWO_PI;
+        const double vw2 = vwx * vwx + vwz * vwz;
+        if (vw2 >= 1e-18) {
+          const double dot = fx * vwx + fz * vwz;
+          g_shed = dot < P.cos_crit * sqrt(vw2);
+          g_rev = dot < 0.0;
         }
         if (lane == 0) {
           ctl->fx = fx; ctl->fz = fz; ctl->nx = nx; ctl->nz = nz; ctl->s = s;
@@ -630,8 +636,8 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           ctl->lz = rz + P.shed_off * fz;
           ctl->tx = (rx - fx * s * nb) - P.shed_off * fx;
           ctl->tz = (rz - fz * s * nb) - P.shed_off * fz;
-          ctl->shed = fabs(aoa) > P.crit_aoa;
-          ctl->rev = fabs(aoa) > 0.5 * PI;
+          ctl->shed = g_shed;
+          ctl->rev = g_rev;
           const double u = feedback ? control_at(a, row, t, ctl->x, ctl->tacc) : u_next;
           ctl->u = clampd(u, -P.u_lim, P.u_lim);
         }
@@ -886,11 +892,11 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           const double d1x = ax1 - ax0, d1z = az1 - az0, d2x = bx1 - bx0, d2z = bz1 - bz0;
           const double den = d1x * d2z - d1z * d2x;
           bool hit = false;
-          if (den != 0.0) {
+          if (den != 0.0) {  // 0 <= num / den <= 1 for both parameters, without dividing
             const double ex = bx0 - ax0, ez = bz0 - az0;
-            const double tt = (ex * d2z - ez * d2x) / den;
-            const double uu = (ex * d1z - ez * d1x) / den;
-            hit = tt >= 0.0 && tt <= 1.0 && uu >= 0.0 && uu <= 1.0;
+            const double nt = ex * d2z - ez * d2x, nu = ex * d1z - ez * d1x;
+            hit = den > 0.0 ? (nt >= 0.0 && nt <= den && nu >= 0.0 && nu <= den)
+                            : (nt <= 0.0 && nt >= den && nu <= 0.0 && nu >= den);
           }
           if (hit) {
             hl[nholes++] = ra;
