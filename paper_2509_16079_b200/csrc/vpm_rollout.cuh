@@ -652,14 +652,19 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
       }
       PHASE_MARK(2);
     }
-    if (pass != D_PASS && conv) {
+    const int wslot = SLOT_REV ? NW - 1 - warp : warp;
+    if (pass != D_PASS && conv && 32 * wslot >= n_live) {
+      // a warp without live targets (small wakes) only clears its merge candidates
+      if (lane == 0)
+        for (int r = 0; r < ctl->mcnt; ++r) cand[warp * MC + r] = 0u;
+    } else if (pass != D_PASS && conv) {
       // ---------------- P2, all warps: S1 convection sweep of step t, then A
       // (reads the raw buffer, writes the other one: no read/write race with
       //  the warps still sweeping, and on a failure in D the raw buffer still
       //  holds the reference's failure-time wake).  Slot k of warp w holds the
-      //  particles c = 32 (NW k + w) + lane; warp 0 takes its slots after D.
+      //  particles c = 32 (NW k + NW-1-w) + lane (the odd block lands on the last
+      //  warp, not on warp 0, which runs D after its slots).
       const int kmax = R;
-      const int wslot = SLOT_REV ? NW - 1 - warp : warp;
       auto slot_base = [&](int k) { return 32 * (NW * k + wslot); };
       float ux[R], uz[R];
       {
