@@ -540,31 +540,69 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
         const double xwx = rx - P.l_w * fx, xwz = rz - P.l_w * fz;
         const double dlev = hp ? (ctl->lev_cur - ctl->lev_prev) * P.inv_dt : 0.0;
 
-        for (int p = lane; p < nb; p += 32) {
-          double uxp, uzp;
-          split_result(red, RS, NSEG, p, uxp, uzp);
-          double cum = 0.0, cum_prev = 0.0;
-          for (int i = 0; i <= p; ++i) { cum += gam[i]; cum_prev += pgp[i]; }
-          const double rate = hp ? (cum - cum_prev) * P.inv_dt + dlev : 0.0;
-          const double e = P.eta * rate + (1.0 - P.eta) * (hp ? ema[p] : 0.0);
-          const double svx = vx + om * (-(bz[p] - rz)), svz = vz + om * (bx[p] - rx);
-          const double beta = (uxp - svx) * fx + (uzp - svz) * fz;
-          const double dp = P.rho * (beta * gam[p] * P.inv_s + e);
-          const double pfx = dp * s * nx, pfz = dp * s * nz;
-          pf[3 * p] = pfx;
-          pf[3 * p + 1] = pfz;
-          pf[3 * p + 2] = (bx[p] - xwx) * pfz - (bz[p] - xwz) * pfx;
-          ema[p] = e;
+        double Fx, Fz, M;
+        if (nb <= 32) {
+          // one panel per lane: the cumulative circulations by a warp scan and the
+          // force / moment sums by a fixed butterfly instead of per-lane serial loops
+          const int p = lane;
+          const bool act = p < nb;
+          double uxp = 0.0, uzp = 0.0;
+          if (act) split_result(red, RS, NSEG, p, uxp, uzp);
+          double cum = act ? gam[p] : 0.0, cum_prev = act ? pgp[p] : 0.0;
+          for (int o = 1; o < nb; o <<= 1) {
+            const double c1 = __shfl_up_sync(0xffffffffu, cum, o);
+            const double c2 = __shfl_up_sync(0xffffffffu, cum_prev, o);
+            if (lane >= o) {
+              cum += c1;
+              cum_prev += c2;
+            }
+          }
+          double pfx = 0.0, pfz = 0.0, pm = 0.0;
+          if (act) {
+            const double rate = hp ? (cum - cum_prev) * P.inv_dt + dlev : 0.0;
+            const double e = P.eta * rate + (1.0 - P.eta) * (hp ? ema[p] : 0.0);
+            const double svx = vx + om * (-(bz[p] - rz)), svz = vz + om * (bx[p] - rx);
+            const double beta = (uxp - svx) * fx + (uzp - svz) * fz;
+            const double dp = P.rho * (beta * gam[p] * P.inv_s + e);
+            pfx = dp * s * nx;
+            pfz = dp * s * nz;
+            pm = (bx[p] - xwx) * pfz - (bz[p] - xwz) * pfx;
+            ema[p] = e;
+          }
+          Fx = warp_sum_d(pfx);
+          Fz = warp_sum_d(pfz);
+          M = warp_sum_d(pm);
+          __syncwarp();
+          PHASE_MARK(9);
+          if (act) { pgp[p] = gam[p]; pxp[p] = bx[p]; pzp[p] = bz[p]; }
+        } else {
+          for (int p = lane; p < nb; p += 32) {
+            double uxp, uzp;
+            split_result(red, RS, NSEG, p, uxp, uzp);
+            double cum = 0.0, cum_prev = 0.0;
+            for (int i = 0; i <= p; ++i) { cum += gam[i]; cum_prev += pgp[i]; }
+            const double rate = hp ? (cum - cum_prev) * P.inv_dt + dlev : 0.0;
+            const double e = P.eta * rate + (1.0 - P.eta) * (hp ? ema[p] : 0.0);
+            const double svx = vx + om * (-(bz[p] - rz)), svz = vz + om * (bx[p] - rx);
+            const double beta = (uxp - svx) * fx + (uzp - svz) * fz;
+            const double dp = P.rho * (beta * gam[p] * P.inv_s + e);
+            const double pfx = dp * s * nx, pfz = dp * s * nz;
+            pf[3 * p] = pfx;
+            pf[3 * p + 1] = pfz;
+            pf[3 * p + 2] = (bx[p] - xwx) * pfz - (bz[p] - xwz) * pfx;
+            ema[p] = e;
+          }
+          __syncwarp();
+          PHASE_MARK(9);
+          for (int p = lane; p < nb; p += 32) { pgp[p] = gam[p]; pxp[p] = bx[p]; pzp[p] = bz[p]; }
+          // wing force / moment sums, one component per lane, panel order as _core.pyx:404-406
+          double fc = 0.0;
+          if (lane < 3)
+            for (int p = 0; p < nb; ++p) fc += pf[3 * p + lane];
+          Fx = __shfl_sync(0xffffffffu, fc, 0);
+          Fz = __shfl_sync(0xffffffffu, fc, 1);
+          M = __shfl_sync(0xffffffffu, fc, 2);
         }
-        __syncwarp();
-        PHASE_MARK(9);
-        for (int p = lane; p < nb; p += 32) { pgp[p] = gam[p]; pxp[p] = bx[p]; pzp[p] = bz[p]; }
-        // wing force / moment sums, one component per lane, panel order as _core.pyx:404-406
-        double fc = 0.0;
-        if (lane < 3)
-          for (int p = 0; p < nb; ++p) fc += pf[3 * p + lane];
-        const double Fx = __shfl_sync(0xffffffffu, fc, 0), Fz = __shfl_sync(0xffffffffu, fc, 1);
-        const double M = __shfl_sync(0xffffffffu, fc, 2);
         if (lane == 0) {
           ctl->fwx = Fx; ctl->fwz = Fz; ctl->mw = M;
           ctl->lev_prev = ctl->lev_cur;
