@@ -172,11 +172,12 @@ int device_sms() {
 // (slot k of warp w = particles 32 (NW k + NW-1-w) .. +31) covering cap + 4 (the
 // largest wake a snapshot may hold), so every particle is a register target.
 // Warp 0 runs the FP64 loads / dynamics / geometry phase after its slots.  NT is
-// the smallest of 64..512 that still puts >= 24 warps on every SM given how many
+// the smallest power of two >= 64 (>= the split-sweep chain count when the launch
+// is latency-bound) that still puts >= 24 warps on every SM given how many
 // rollouts each SM receives (4097 rollouts on one GPU -> 128 x 5, 512 per GPU at
 // 8 GPUs -> 256 x 3).  Results do not depend on the shape (canonical reduction
 // orders, see vpm_rollout.cuh).  VPM_SHAPE="nt,r" / VPM_MAXREG override for tuning.
-Shape pick_shape(int cap, int rows) {
+Shape pick_shape(int cap, int nb, int rows) {
   const int need = cap + 4;
   if (const char *e = getenv("VPM_SHAPE")) {
     Shape s{0, 0, 0, 64};
@@ -187,8 +188,15 @@ Shape pick_shape(int cap, int rows) {
     }
   }
   const double per_sm = rows > 0 ? (double)rows / device_sms() : 1.0;
+  // latency-bound launches (<= 8 rollouts per SM): at least one thread per
+  // (target, segment) chain of the split sweeps (nb x NSEG, capped at 256), which
+  // are then the step's critical path (C2, cap 60: 64 -> 128 threads is 0.40 ->
+  // 0.34 ms); throughput-bound launches keep the tightest tile
+  int nt0 = 64;
+  if (per_sm <= 8.0)
+    while (nt0 < 256 && nt0 < nb * vpm::NSEG) nt0 *= 2;
   Shape best{512, 8, 0, 64};
-  for (int nt = 64; nt <= 512; nt *= 2) {
+  for (int nt = nt0; nt <= 512; nt *= 2) {
     const int r = (need + nt - 1) / nt;
     if (r > 8) continue;
     best = Shape{nt, r, 0, 64};
@@ -236,7 +244,7 @@ cudaError_t launch_r(const Args &a, int grid, const Shape &sh, size_t smem, cuda
 }
 
 cudaError_t launch_rollouts(Args a, int grid, cudaStream_t st) {
-  const Shape sh = pick_shape(a.P.cap, grid);
+  const Shape sh = pick_shape(a.P.cap, a.P.nb, grid);
   const size_t smem = vpm::make_layout(a.P.cap, a.P.nb, sh.nt).total;
   switch (sh.minb) {
     case 48: return launch_r<48>(a, grid, sh, smem, st);
@@ -337,7 +345,7 @@ extern "C" {
 const char *vpm_last_error(void) { return g_err.c_str(); }
 
 int vpm_launch_shape(int cap, int nb, int rows, int *threads, int *targets, int *smem_bytes) {
-  const Shape s = pick_shape(cap, rows);
+  const Shape s = pick_shape(cap, nb, rows);
   if (threads) *threads = s.nt;
   if (targets) *targets = s.r;
   if (smem_bytes) *smem_bytes = vpm::make_layout(cap, nb, s.nt).total;
