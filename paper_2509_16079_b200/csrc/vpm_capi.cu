@@ -188,21 +188,30 @@ Shape pick_shape(int cap, int nb, int rows) {
     }
   }
   const double per_sm = rows > 0 ? (double)rows / device_sms() : 1.0;
-  // latency-bound launches (<= 8 rollouts per SM): at least one thread per
-  // (target, segment) chain of the split sweeps (nb x NSEG, capped at 256), which
-  // are then the step's critical path (C2, cap 60: 64 -> 128 threads is 0.40 ->
-  // 0.34 ms); throughput-bound launches keep the tightest tile
-  int nt0 = 64;
-  if (per_sm <= 8.0)
-    while (nt0 < 256 && nt0 < nb * vpm::NSEG) nt0 *= 2;
   Shape best{512, 8, 0, 64};
-  for (int nt = nt0; nt <= 512; nt *= 2) {
-    const int r = (need + nt - 1) / nt;
-    if (r > 8) continue;
-    best = Shape{nt, r, 0, 64};
-    if (nt >= need) break;  // more lanes than particles
-    const double ctas = per_sm < 1024.0 / nt ? per_sm : 1024.0 / nt;
-    if (ctas * nt >= 768.0) break;
+  if (per_sm <= 8.0) {
+    // latency-bound launch (one round): the per-rollout critical path matters, so
+    // about two 32-particle blocks per warp (the largest NT with need >= 2 NT) and
+    // at least one thread per (target, segment) chain of the split sweeps (nb x
+    // NSEG, capped at 256).  Measured: C2 (cap 60) 64 -> 128 threads 0.40 -> 0.34
+    // ms; cap 512 at 513 / 1025 rows 256 x 3 beats 128 x 5 by 10% / 8%; cap 256 at
+    // 1025 rows 128 x 3 beats 256 x 2 by 20%.
+    int nt = 64;
+    while (nt < 512 && need >= 4 * nt) nt *= 2;
+    int nt0 = 64;
+    while (nt0 < 256 && nt0 < nb * vpm::NSEG) nt0 *= 2;
+    if (nt < nt0) nt = nt0;
+    best = Shape{nt, (need + nt - 1) / nt, 0, 64};
+  } else {
+    // throughput-bound: the tightest tile that still keeps >= 24 warps per SM
+    for (int nt = 64; nt <= 512; nt *= 2) {
+      const int r = (need + nt - 1) / nt;
+      if (r > 8) continue;
+      best = Shape{nt, r, 0, 64};
+      if (nt >= need) break;  // more lanes than particles
+      const double ctas = per_sm < 1024.0 / nt ? per_sm : 1024.0 / nt;
+      if (ctas * nt >= 768.0) break;
+    }
   }
   // Wave quantisation: with c CTAs resident per SM a launch takes ~ceil(n/c) rounds
   // of c rollouts per SM.  For 128-thread CTAs, 72 registers (7 CTAs/SM) instead of
