@@ -285,6 +285,46 @@ def extras(torch, dev, sc, flat, plan, mp):
     return out
 
 
+def c5_sharded(torch, dev, rank, world):
+    """C5 (Biot-Savart stress, K=16384 rollouts x H=5, attached flow) with the
+    rollouts sharded over the ranks; device time max over ranks, interactions
+    summed; fraction of world x FP32 peak."""
+    import torch.distributed as dist
+    from paper_2509_16079_b200 import config
+    from paper_2509_16079_b200.device import DevicePlan
+    from paper_2509_16079_b200.sharding import row_range
+    K5, H5 = 16384, 5
+    b, e = row_range(K5, world, rank)
+    res = {}
+    for N in (512, 2048):
+        rng = np.random.default_rng(1000 + N)  # same wake on every rank
+        v = config.VpmConfig(particle_cap=N)
+        ip, fp = config.pack_params(v, config.GliderParams())
+        p5 = DevicePlan(ip, fp, device=dev.index)
+        wp = rng.normal(0.0, 0.5, (N, 2))
+        wp[:, 0] -= 3.0
+        p5.set_fluid((wp, rng.normal(0.0, 0.05, N), np.zeros(N, np.int64), N, -1, -1,
+                      np.zeros((10, 2)), np.zeros(10), 0, 0.0, np.zeros(10)))
+        x5 = torch.tensor([0.0, 0.0, 0.0, 0.0, 7.0, 0.0, 0.0], dtype=torch.float64, device=dev)
+        ctrl = torch.zeros(e - b, H5, dtype=torch.float64, device=dev)
+        o5 = {"status": torch.empty(e - b, dtype=torch.int64, device=dev),
+              "finals": torch.empty(e - b, 7, dtype=torch.float64, device=dev),
+              "interactions": torch.zeros(e - b, dtype=torch.int64, device=dev)}
+        ms = _time_ms(torch, lambda: p5.batch(x5, H5, controls=ctrl, rows=e - b, out=o5))
+        st = torch.tensor([ms, float(o5["interactions"].sum().item())], dtype=torch.float64, device=dev)
+        if world > 1:
+            mx, sm = st.clone(), st.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+            ms, inter = float(mx[0]), float(sm[1])
+        else:
+            inter = float(st[1])
+        tf = 12.0 * inter / (ms * 1e-3) / 1e12
+        res[str(N)] = {"ms": ms, "tflops": tf, "frac_of_fp32_peak": tf / (world * FP32_SPEC_TFLOPS),
+                       "rows_per_rank": e - b}
+    return {"K": K5, "H": H5, "n_gpus": world, "by_N": res}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -395,6 +435,38 @@ def run_ours(args):
                "set_fluid_ms": 1e3 * split[0] / args.steps,
                "optimize_ms": 1e3 * split[1] / args.steps}
 
+    elif world > 1:
+        # the sharded planner's public API with host buffers: every step copies this
+        # rank's noise rows from pinned memory and reads u* back; wall time, max over ranks
+        lo, hi = max(mp.begin - 1, 0), mp.end - 1  # noise row of global row g is g - 1
+        pin = torch.empty((args.steps, hi - lo, HORIZON), dtype=torch.float64).pin_memory()
+        for s in range(args.steps):
+            pin[s].copy_(noise_all[args.warmup + s][lo:hi])
+        dnoise = torch.zeros((K_SAMPLES, HORIZON), dtype=torch.float64, device=dev)
+        u_back = torch.empty(HORIZON, dtype=torch.float64).pin_memory()
+
+        def one_sh(s):
+            dnoise[lo:hi].copy_(pin[s], non_blocking=True)
+            mp.set_noise(dnoise)
+            mp.iteration()
+            u_back.copy_(mp.ustar)  # D2H of the step's result (synchronising)
+
+        one_sh(0)
+        dist.barrier()
+        t0 = time.perf_counter()
+        for s in range(args.steps):
+            one_sh(s)
+        dist.barrier()
+        wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+        e2e_s = float(wall[0])
+        e2e = {"value": B * args.steps / e2e_s, "unit": "rollouts/s",
+               "h2d_bytes_per_step": K_SAMPLES * HORIZON * 8, "d2h_bytes_per_step": world * HORIZON * 8,
+               "ms_per_step": 1e3 * e2e_s / args.steps,
+               "path": "ShardedMppi per rank: pinned H2D of the rank's noise rows, iteration "
+                       "(rollouts + partial + all_gather + combine), D2H of u*; max over ranks"}
+
+    c5 = c5_sharded(torch, dev, rank, world)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -426,6 +498,7 @@ def run_ours(args):
                          "achieved_frac_of_ceiling": (achieved / mix_ceiling) if achieved else None,
                          "source": "probe of the direct kernel's instruction mix (8 FP32 lane-ops + "
                                    "1 MUFU.RSQ per interaction, independent chains, no loads)"}},
+        "c5_sharded": c5,
         "gpu_launches": ShardedMppi.kernels_per_iteration * args.steps,
         "clocks": clk.summary(),
     }
