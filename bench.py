@@ -466,7 +466,7 @@ def run_ours(args):
                "path": "ShardedMppi per rank: pinned H2D of the rank's noise rows, iteration "
                        "(rollouts + partial + all_gather + combine), D2H of u*; max over ranks"}
 
-    c5 = c5_sharded(torch, dev, rank, world)
+    c5 = None if args.no_c5 else c5_sharded(torch, dev, rank, world)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -520,6 +520,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-c5", action="store_true", help="skip the sharded C5 stress measurement")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the C2 / policy / C5 Biot-Savart sweep side measurements")
     args = ap.parse_args()
