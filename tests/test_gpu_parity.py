@@ -464,3 +464,31 @@ def test_optimize_pipeline_equals_host_entry_and_rewinds_on_failure(torch_cuda):
         mppi.optimize(bad, fl, sc["warm"], mcfg, eng, rng)
     twin.normal(0.0, 1.0, (256, 50))
     assert rng.bit_generator.state == twin.bit_generator.state
+
+
+@pytest.mark.parametrize("N", [1024, 2048])
+def test_c5_large_wake_vs_oracle(torch_cuda, oracle_core, N):
+    """C5-scale wakes (N = 1024 / 2048, random wake, attached flow so N
+    stays fixed; launch shapes 512 x 3 / 512 x 5): a few rollouts of 5 steps
+    against the FP64 oracle on identical inputs -- final states, and the wake the
+    single-rollout path returns."""
+    from paper_2509_16079_b200 import config, rollout, vpm
+    rng = np.random.default_rng(N)
+    v = config.VpmConfig(particle_cap=N)
+    eng = rollout.Engine(v, config.GliderParams())
+    fl = vpm.FluidState.empty(v)
+    fl.wake_pos[:N] = rng.normal(0.0, 0.5, (N, 2)) - np.array([3.0, 0.0])
+    fl.wake_gamma[:N] = rng.normal(0.0, 0.05, N)
+    fl.n_wake = N
+    x0 = np.array([0.0, 0.0, 0.0, 0.0, 7.0, 0.0, 0.0])
+    ctrl = np.clip(rng.normal(0.0, 3.0, (4, 5)), -15, 15)
+    res = eng.batch(rollout.RolloutRequest(x0=x0, fluid=fl, controls=ctrl, record=True))
+    d = oracle_core.batch_rollout_diag(x0, ctrl, *fl.flat(), eng.iparams, eng.fparams, record=True)
+    np.testing.assert_array_equal(res.status, d["status"])
+    assert (res.status == 0).all()
+    assert_close(res.trajectories, d["trajs"], what=f"C5 N={N} trajs")
+    rc, _, fl_g = eng.rollout(x0, ctrl[0], fl)
+    rc_o, _, flat_o = oracle_core.rollout(x0, ctrl[0], *fl.flat(), eng.iparams, eng.fparams, False, True)
+    assert rc == rc_o == 0 and fl_g.n_wake == flat_o[3] == N
+    np.testing.assert_array_equal(fl_g.wake_age[:N], flat_o[2][:N])
+    assert_close(fl_g.wake_pos[:N], flat_o[0][:N], what=f"C5 N={N} wake")
