@@ -290,8 +290,9 @@ struct vpm_plan {
   double *d_plev = nullptr;
   int n_wake = 0, ring_a = -1, ring_b = -1, n_prev = 0;
   double prev_lev = 0.0;
-  double *d_wbuf = nullptr;
+  double *d_wbuf = nullptr;  // chunk partials of the MPPI softmax reduction
   size_t wbuf_len = 0;
+  unsigned *d_ticket = nullptr;  // last-CTA ticket of the chunked reduction (re-armed by it)
   // rollout-kernel timing
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // start/stop pairs
@@ -414,6 +415,7 @@ void vpm_plan_destroy(vpm_plan *p) {
   cudaFree(p->d_scal);
   cudaFree(p->d_plev);
   cudaFree(p->d_wbuf);
+  cudaFree(p->d_ticket);
   cudaFree(p->hscratch);
   if (p->hstream) cudaStreamDestroy(p->hstream);
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
@@ -570,18 +572,25 @@ int vpm_mppi_partial(vpm_plan *p, const double *d_cost, int rows, int row_begin,
   if (temperature <= 0.0) return fail_cfg("temperature must be > 0");
   std::lock_guard<std::mutex> lk(p->mu);
   CK(cudaSetDevice(p->device));
-  if (p->wbuf_len < (size_t)rows) {
+  const int G = rows > 0 ? (rows + vpm::PCH_ROWS - 1) / vpm::PCH_ROWS : 1;
+  const size_t need = (size_t)G * (T + 2);
+  if (p->wbuf_len < need) {
     cudaFree(p->d_wbuf);
     p->d_wbuf = nullptr;
-    CK(cudaMalloc(&p->d_wbuf, sizeof(double) * (size_t)(rows > 1 ? rows : 1)));
-    p->wbuf_len = rows;
+    CK(cudaMalloc(&p->d_wbuf, sizeof(double) * need));
+    p->wbuf_len = need;
   }
-  constexpr int NTH = 512;
-  const size_t smem = sizeof(double) * ((NTH / 32) * (size_t)T + 2 * (NTH / 32));
+  if (!p->d_ticket) {
+    CK(cudaMalloc(&p->d_ticket, sizeof(unsigned)));
+    CK(cudaMemset(p->d_ticket, 0, sizeof(unsigned)));
+  }
+  const size_t smem = sizeof(double) * ((size_t)vpm::PCH_WARPS * T + 2 * vpm::PCH_WARPS + G);
   if (smem > 48 * 1024)
-    CK(cudaFuncSetAttribute(vpm::mppi_partial_kernel<NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  vpm::mppi_partial_kernel<NTH><<<1, NTH, smem, (cudaStream_t)stream>>>(
-      d_cost, rows, row_begin, d_ustar, d_noise, sigma, p->P.u_lim, T, temperature, p->d_wbuf, d_partial);
+    CK(cudaFuncSetAttribute(vpm::mppi_partial_chunked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+  vpm::mppi_partial_chunked_kernel<<<G, 32 * vpm::PCH_WARPS, smem, (cudaStream_t)stream>>>(
+      d_cost, rows, row_begin, d_ustar, d_noise, sigma, p->P.u_lim, T, temperature, p->d_wbuf, p->d_ticket,
+      d_partial);
   CK(cudaGetLastError());
   return VPM_OK;
 }

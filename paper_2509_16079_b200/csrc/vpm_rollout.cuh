@@ -1048,89 +1048,105 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
 }
 
 // ---- MPPI reductions -----------------------------------------------------------------
-// Partial softmax sums of one shard (mppi.py:46-59): part = {J_min, Z, S[0..T)}.
-template <int NTH>
-__global__ void __launch_bounds__(NTH) mppi_partial_kernel(const double *__restrict__ cost, int rows,
-                                                            int row_begin, const double *__restrict__ ustar,
-                                                            const double *__restrict__ noise, double sigma,
-                                                            double ulim, int T, double lambda,
-                                                            double *__restrict__ wbuf,
-                                                            double *__restrict__ part) {
-  constexpr int NW = NTH / 32;
-  extern __shared__ double sh[];  // NW * T + 2 * NW
-  double *sacc = sh;              // [NW][T]
-  double *sred = sh + NW * T;     // [2 NW]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // J_min over finite costs
-  double jm = INFINITY;
-  for (int r = tid; r < rows; r += NTH) {
-    const double J = cost[r];
-    if (isfinite(J) && J < jm) jm = J;
-  }
-  for (int o = 16; o >= 1; o >>= 1) jm = fmin(jm, __shfl_xor_sync(0xffffffffu, jm, o));
+// Chunked softmax partials of one shard (mppi.py:46-59), a streaming kernel: CTA c
+// owns rows [c CH, c CH + CH) -- each warp 8 consecutive rows, whose control rows
+// (clip(u* + sigma noise), coalesced over t) it loads all at once -- and writes the
+// chunk partial {J_min_c, Z_c, S_c[T]} (weights relative to J_min_c).  The last CTA
+// to finish (ticket) combines the chunk partials in chunk order, rescaled to the
+// shard minimum, into part = {J_min, Z, S[T]}, and re-arms the ticket.  Every sum
+// has a fixed order, so the result does not depend on scheduling.
+constexpr int PCH_WARPS = 8, PCH_ROWS = 8 * PCH_WARPS;  // 256 threads, 64 rows per CTA
+__global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
+    const double *__restrict__ cost, int rows, int row_begin, const double *__restrict__ ustar,
+    const double *__restrict__ noise, double sigma, double ulim, int T, double lambda,
+    double *__restrict__ chunks, unsigned *__restrict__ ticket, double *__restrict__ part) {
+  extern __shared__ double sh[];  // [PCH_WARPS][T] control sums, 2 PCH_WARPS, [G] scales
+  double *sacc = sh, *sred = sh + PCH_WARPS * T;
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ld = T + 2;
+  const int rw = blockIdx.x * PCH_ROWS + warp * 8;  // this warp's first row
+  // costs of the warp's 8 rows (lane j < 8 holds row j)
+  const double Jl = (lane < 8 && rw + lane < rows) ? cost[rw + lane] : INFINITY;
+  double jm = isfinite(Jl) ? Jl : INFINITY;
+  for (int o = 4; o >= 1; o >>= 1) jm = fmin(jm, __shfl_xor_sync(0xffffffffu, jm, o));
   if (lane == 0) sred[warp] = jm;
   __syncthreads();
   jm = INFINITY;
-  for (int w = 0; w < NW; ++w) jm = fmin(jm, sred[w]);
-  __syncthreads();
+  for (int w = 0; w < PCH_WARPS; ++w) jm = fmin(jm, sred[w]);  // chunk minimum (exact)
   const bool any = isfinite(jm);
-  // weights and normaliser
-  double z = 0.0;
-  for (int r = tid; r < rows; r += NTH) {
-    const double J = cost[r];
-    const double w = (any && isfinite(J)) ? exp(-(J - jm) / lambda) : 0.0;
-    wbuf[r] = w;
-    z += w;
-  }
-  z = warp_sum_d(z);
-  if (lane == 0) sred[NW + warp] = z;
-  __syncthreads();
-  // weighted control sums S[t] = sum_r w_r u_r[t]: warp w takes the 32-row blocks
-  // w, w+NW, ... in row order; lanes own steps t = tc + lane, tc + 32 + lane with
-  // the accumulators in registers; 8 rows' control loads are in flight at once
-  // (rows with w = 0 load nothing and add an exact 0)
+  const double wl = (any && isfinite(Jl)) ? exp(-(Jl - jm) / lambda) : 0.0;
+  double z = wl;  // lanes >= 8 hold 0; fixed butterfly over the 8 rows
+  for (int o = 4; o >= 1; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+  double wr[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) wr[j] = __shfl_sync(0xffffffffu, wl, j);
   for (int tc = 0; tc < T; tc += 64) {
     const int t0 = tc + lane, t1 = tc + 32 + lane;
     const double us0 = t0 < T ? ustar[t0] : 0.0, us1 = t1 < T ? ustar[t1] : 0.0;
-    double acc0 = 0.0, acc1 = 0.0;
-    for (int base = 32 * warp; base < rows; base += 32 * NW) {
-      const int r = base + lane;
-      const double wl = r < rows ? wbuf[r] : 0.0;
-      for (int i = 0; i < 32; i += 8) {
-        double w[8], u0[8], u1[8];
+    double u0[8], u1[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          w[j] = __shfl_sync(0xffffffffu, wl, i + j);
-          const int g = row_begin + base + i + j;
-          u0[j] = us0;
-          u1[j] = us1;
-          if (w[j] != 0.0 && g > 0) {
-            const double *nz = noise + (size_t)(g - 1) * T;
-            if (t0 < T) u0[j] = clampd(us0 + nz[t0] * sigma, -ulim, ulim);
-            if (t1 < T) u1[j] = clampd(us1 + nz[t1] * sigma, -ulim, ulim);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          acc0 += w[j] * u0[j];
-          acc1 += w[j] * u1[j];
-        }
+    for (int j = 0; j < 8; ++j) {  // all loads of the 8 rows first
+      const int g = row_begin + rw + j;
+      u0[j] = us0;
+      u1[j] = us1;
+      if (wr[j] != 0.0 && g > 0) {
+        const double *nz = noise + (size_t)(g - 1) * T;
+        if (t0 < T) u0[j] = clampd(us0 + nz[t0] * sigma, -ulim, ulim);
+        if (t1 < T) u1[j] = clampd(us1 + nz[t1] * sigma, -ulim, ulim);
       }
     }
-    if (t0 < T) sacc[warp * T + t0] = acc0;
-    if (t1 < T) sacc[warp * T + t1] = acc1;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // row order
+      a0 += wr[j] * u0[j];
+      a1 += wr[j] * u1[j];
+    }
+    if (t0 < T) sacc[warp * T + t0] = a0;
+    if (t1 < T) sacc[warp * T + t1] = a1;
+  }
+  if (lane == 0) sred[PCH_WARPS + warp] = z;
+  __syncthreads();
+  double *mine = chunks + (size_t)blockIdx.x * ld;
+  if (threadIdx.x == 0) {
+    double Z = 0.0;
+    for (int w = 0; w < PCH_WARPS; ++w) Z += sred[PCH_WARPS + w];
+    mine[0] = jm;
+    mine[1] = Z;
+  }
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    double S = 0.0;
+    for (int w = 0; w < PCH_WARPS; ++w) S += sacc[w * T + t];
+    mine[2 + t] = S;
+  }
+  // last CTA: combine the chunks in chunk order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int G = gridDim.x;
+  const volatile double *vc = chunks;  // written by other SMs: bypass L1
+  double *scale = sred + 2 * PCH_WARPS;  // [G]
+  double gm = INFINITY;
+  for (int c = 0; c < G; ++c) gm = fmin(gm, vc[(size_t)c * ld]);
+  for (int c = threadIdx.x; c < G; c += blockDim.x) {
+    const double jc = vc[(size_t)c * ld];
+    scale[c] = (isfinite(gm) && isfinite(jc)) ? exp(-(jc - gm) / lambda) : 0.0;
   }
   __syncthreads();
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     double Z = 0.0;
-    for (int w = 0; w < NW; ++w) Z += sred[NW + w];
-    part[0] = jm;
+    for (int c = 0; c < G; ++c) Z += vc[(size_t)c * ld + 1] * scale[c];
+    part[0] = gm;
     part[1] = Z;
+    *ticket = 0u;
   }
-  for (int t = tid; t < T; t += NTH) {
-    double s = 0.0;
-    for (int w = 0; w < NW; ++w) s += sacc[w * T + t];
-    part[2 + t] = s;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    double S = 0.0;
+    for (int c = 0; c < G; ++c) S += vc[(size_t)c * ld + 2 + t] * scale[c];
+    part[2 + t] = S;
   }
 }
 
