@@ -36,6 +36,13 @@ def gather_partials(partial, group=None):
     out = torch.empty((W, flat.numel()), dtype=partial.dtype, device=partial.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, flat, group=group)   # one NCCL all-gather
+    elif flat.is_cuda:
+        # gloo has no all_gather for CUDA tensors: gather through host memory
+        # (functional multi-process tests on one device; 416 bytes per rank)
+        host = flat.cpu()
+        parts = [torch.empty_like(host) for _ in range(W)]
+        dist.all_gather(parts, host, group=group)
+        out.copy_(torch.stack(parts))
     else:
         dist.all_gather(list(out.unbind(0)), flat, group=group)
     return out

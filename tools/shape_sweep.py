@@ -1,5 +1,5 @@
 """Time one C4 candidate batch (K=4096+1, H=50, N=512 + ring) of the rollout kernel
-under different launch shapes (VPM_SHAPE="nt,r,w0", VPM_MINB) -- a tuning tool;
+under different launch shapes (VPM_SHAPE="nt,r,w0", VPM_MAXREG) -- a tuning tool;
 results are shape-independent, only the time changes."""
 import json
 import os
@@ -30,13 +30,13 @@ xp = f64([3.5, 0, np.pi / 4, 0, 0.5, -0.5, 0])
 x0, us = f64(sc["x0"]), f64(sc["warm"])
 ref = None
 for shp in shapes:
-    for key in ("VPM_SHAPE", "VPM_MINB"):
+    for key in ("VPM_SHAPE", "VPM_MAXREG"):
         os.environ.pop(key, None)
     if shp != "default":
         parts = shp.split("/")
         os.environ["VPM_SHAPE"] = parts[0]
         if len(parts) > 1:
-            os.environ["VPM_MINB"] = parts[1]
+            os.environ["VPM_MAXREG"] = parts[1]
     out = None
     for _ in range(2):
         out = plan.batch(x0, 50, ustar=us, noise=noise, sigma=2.0, rows=K + 1, q=q, x_perch=xp, out=out)
