@@ -63,7 +63,10 @@ constexpr int NB_MAX = 64;     // reference MAXNB (_core.pyx:23)
 constexpr int NT_MAX = 512;    // threads per rollout CTA
 constexpr int NW_MAX = NT_MAX / 32;
 constexpr int MC = 8;          // merge candidates kept per warp
-constexpr int NSEG = 12;       // source segments of the split sweeps (fixed: canonical order)
+#ifndef VPM_NSEG
+#define VPM_NSEG 12
+#endif
+constexpr int NSEG = VPM_NSEG;  // source segments of the split sweeps (fixed: canonical order)
 constexpr int HOLES_MAX = 16;
 constexpr int WAKE_PAD = 8;    // wake slots beyond cap (reference buffers hold cap+4)
 #ifndef VPM_SWEEP_UNROLL

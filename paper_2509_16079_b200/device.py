@@ -17,6 +17,7 @@ compute is in ``libvpm_b200.so``.  :class:`DevicePlan` exposes the layer-2 C ABI
 from __future__ import annotations
 
 import ctypes as C
+import threading
 
 import numpy as np
 
@@ -57,6 +58,10 @@ class DevicePlan:
         if not h:
             raise ValueError(f"vpm_plan_create: {_lib.last_error()}")
         self.handle = C.c_void_p(h)
+        # the snapshot and the pinned staging buffer are per-plan state: host-side
+        # sequences that set the snapshot and queue launches reading it (optimize,
+        # replan, build_policy) hold this lock, so concurrent callers serialise
+        self.lock = threading.RLock()
         self.nb = int(self.iparams[0])
         self.cap = int(self.iparams[1])
 

@@ -72,6 +72,11 @@ def optimize(x0, fluid: FluidState, warm_start, cfg: MppiConfig, engine: Engine,
         return u
     import torch
     plan = engine_plan(engine)
+    with plan.lock:
+        return _optimize_locked(torch, plan, x0, fluid, u, cfg, rng, iters, H, K)
+
+
+def _optimize_locked(torch, plan, x0, fluid, u, cfg, rng, iters, H, K):
     dev = torch.device("cuda", plan.device)
     plan.set_fluid(fluid)
     n_it = K * H

@@ -53,6 +53,11 @@ def project_forward(policy: Policy, x, fluid: FluidState, t: float, t_proj: int,
     """Advance the snapshot t_proj closed-loop steps under the policy (nmpc.py:88-103).
     Returns (x, fluid, t) or None on failure."""
     torch, plan, dev, f64 = _dev(engine)
+    with plan.lock:
+        return _project_locked(plan, f64, policy, x, fluid, t, t_proj, engine)
+
+
+def _project_locked(plan, f64, policy, x, fluid, t, t_proj, engine):
     plan.set_fluid(fluid)
     nom = policy.nominal
     status, final = plan.project(f64(x), int(t_proj), f64(policy.gains), f64(nom.states),
@@ -80,6 +85,11 @@ def replan(req: ReplanRequest, cfg: ExperimentConfig, engine: Engine,
     caller's generator ends in the reference's state either way.
     """
     torch, plan, dev, f64 = _dev(engine)
+    with plan.lock:
+        return _replan_locked(torch, plan, dev, f64, req, cfg, engine, rng)
+
+
+def _replan_locked(torch, plan, dev, f64, req, cfg, engine, rng):
     dt = engine.cfg.dt
     lim = engine.params.u_limit
     old = req.policy.nominal

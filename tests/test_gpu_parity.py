@@ -437,6 +437,42 @@ def test_concurrent_callers_get_independent_results(torch_cuda):
             np.testing.assert_array_equal(x, y)
 
 
+def test_concurrent_optimize_on_one_engine(torch_cuda):
+    """mppi.optimize / build_policy share the engine's device plan (snapshot and
+    pinned staging); concurrent callers on one engine serialise on the plan's lock
+    and get exactly their serial results."""
+    import threading
+
+    from paper_2509_16079_b200 import config, mppi, rollout, vpm
+    cfg = config.ExperimentConfig()
+    cfg.mppi.batch = 128
+    eng = rollout.Engine.from_config(cfg)
+    x0 = np.array([0.0, 0.0, 0.3, 0.0, 7.0, 0.0, 0.0])
+    ring = vpm.RingDisturbance.from_speed([1.0, -0.1], 7.5, 0.28, 0.02, -1.0)
+    fluids = [vpm.FluidState.empty(cfg.vpm), vpm.inject_ring(vpm.FluidState.empty(cfg.vpm), ring)]
+
+    def job(i):
+        rng = np.random.default_rng(40 + i)
+        return mppi.optimize(x0, fluids[i % 2], np.full(cfg.mppi.horizon, -6.0), cfg.mppi, eng, rng,
+                             iterations=2)
+
+    serial = [job(i) for i in range(4)]
+    got = [None] * 4
+
+    def run(i):
+        for _ in range(3):
+            got[i] = job(i)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for a, b in zip(serial, got):
+        np.testing.assert_array_equal(a, b)
+    assert not np.array_equal(serial[0], serial[1])
+
+
 def test_optimize_pipeline_equals_host_entry_and_rewinds_on_failure(torch_cuda):
     """mppi.optimize (per-iteration draws overlapped with the device) returns bitwise
     what the all-up-front C entry point vpm_mppi_optimize_host returns, and when
