@@ -7,6 +7,7 @@
 // rollout / batch_rollout.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -213,13 +214,35 @@ Shape pick_shape(int cap, int nb, int rows) {
       if (ctas * nt >= 768.0) break;
     }
   }
-  // Wave quantisation: with c CTAs resident per SM a launch takes ~ceil(n/c) rounds
-  // of c rollouts per SM.  For 128-thread CTAs, 72 registers (7 CTAs/SM) instead of
-  // 64 (8 CTAs/SM) when that needs fewer rollout-slots in total (4097 rows on 148
-  // SMs: 28 per SM -> 4 x 7 = 28 instead of 4 x 8 = 32).
-  if (best.nt == 128) {
-    const int n_sm = (int)ceil(per_sm);
-    if (n_sm >= 8 && ((n_sm + 6) / 7) * 7 < ((n_sm + 7) / 8) * 8) best.minb = 72;
+  // Wave quantisation: with c CTAs resident per SM (register-limited) a
+  // throughput-bound launch costs ~ceil(n/c) * c rollout-slots per SM, whatever c
+  // is.  Among the 64 / 72 / 80-register variants take the fewest slots, ties to
+  // the larger register budget (the sweep interleaves more chains).  4097 rows on
+  // 148 SMs (28 per SM): 128 threads at 72 registers = 4 x 7 = 28 slots instead of
+  // 4 x 8 = 32; C5 (16384 rows, 111 per SM) at N = 512: 112 slots either way, 72
+  // registers 3.5% faster; at N = 1024 (256 threads) 72 registers (3 CTAs/SM) 1.5%
+  // faster than 64 (4 CTAs/SM).  Variants that leave fewer than 3 CTAs per SM are
+  // excluded (N = 2048, 512 threads: 1 CTA/SM at 72 registers is 8% slower than 2
+  // at 64), and 64-thread CTAs keep 64 (N = 256: 72 registers 2% slower at equal
+  // slots).  Latency-bound launches (one round) keep 64.
+  const int n_sm = (int)ceil(per_sm);
+  if (per_sm > 8.0 && best.nt >= 128) {
+    const size_t smem = vpm::make_layout(cap, nb, best.nt).total + 1024;
+    auto slots = [&](int regs, int min_c) {
+      int c = 65536 / (best.nt * regs);
+      c = std::min(c, 2048 / best.nt);
+      c = std::min(c, 32);
+      c = std::min(c, (int)((228 * 1024) / smem));
+      return c < min_c ? 1 << 30 : ((n_sm + c - 1) / c) * c;
+    };
+    int bs = slots(64, 1);
+    for (int regs : {72, 80}) {
+      const int sl = slots(regs, 3);
+      if (sl <= bs) {
+        bs = sl;
+        best.minb = regs;
+      }
+    }
   }
   if (const char *m = getenv("VPM_MAXREG")) best.minb = atoi(m);
   return best;
