@@ -16,7 +16,7 @@ torch.cuda.set_device(0)
 dev = torch.device("cuda")
 N = int(sys.argv[1])
 shapes = sys.argv[2].split(";") if len(sys.argv) > 2 else ["default"]
-K5, H5 = 16384, 5
+K5, H5 = int(os.environ.get("C5_K", "16384")), int(os.environ.get("C5_H", "5"))
 rng = np.random.default_rng(11)
 v = config.VpmConfig(particle_cap=N)
 ip, fp = config.pack_params(v, config.GliderParams())
