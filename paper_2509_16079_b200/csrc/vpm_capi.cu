@@ -995,8 +995,15 @@ int vpm_policy_fit(const double *d_nom_x, const double *d_nom_u, const double *d
   a.flag = d_flag;
   a.do_fit = do_fit;
   a.do_riccati = do_riccati;
-  vpm::policy_kernel<<<1, 512, 0, (cudaStream_t)stream>>>(a);
-  CK(cudaGetLastError());
+  if (do_fit) {
+    const int grid = (H + vpm::PFIT_WARPS - 1) / vpm::PFIT_WARPS;
+    vpm::policy_fit_kernel<<<grid, 32 * vpm::PFIT_WARPS, 0, (cudaStream_t)stream>>>(a);
+    CK(cudaGetLastError());
+  }
+  if (do_riccati) {
+    vpm::riccati_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(a);
+    CK(cudaGetLastError());
+  }
   return VPM_OK;
 }
 

@@ -1218,13 +1218,16 @@ __device__ __forceinline__ void cloud_row(const PolicyArgs &p, int i, int k, con
 // solved by Cholesky (the scaling keeps the squared condition number small; SURVEY
 // 7.3.6).  Euler discretisation with the analytic kinematic rows
 // (assemble_discrete, policy.py:121-138).
-// Phase 2, warp 0: backward Riccati recursion S_N = Q_f, h_k = (b'S A)/(r + b'S b),
-// S <- Q + A'S A - (A'S b) h', symmetrised (tvlqr_backward, policy.py:206-233).
-__global__ void __launch_bounds__(512) policy_kernel(const PolicyArgs p) {
-  __shared__ double S[49], SA[49], A[49], Sn[49], bv[7], Sb[7], bS[7], AtSb[7], hh[7];
+// The steps are independent: they are spread over the whole GPU (PFIT_WARPS warps
+// per CTA, ceil(H / PFIT_WARPS) CTAs) -- one CTA of 16 warps took 5 rounds on one SM.
+// Phase 2 (riccati_kernel, one warp, launched after): backward Riccati recursion
+// S_N = Q_f, h_k = (b'S A)/(r + b'S b), S <- Q + A'S A - (A'S b) h', symmetrised
+// (tvlqr_backward, policy.py:206-233).
+constexpr int PFIT_WARPS = 2;
+__global__ void __launch_bounds__(32 * PFIT_WARPS) policy_fit_kernel(const PolicyArgs p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
-  if (p.do_fit) {
-    for (int k = warp; k < p.H; k += NW) {
+  {
+    for (int k = blockIdx.x * NW + warp; k < p.H; k += gridDim.x * NW) {
       const double *nk = p.nom_x + (size_t)k * 7, *nk1 = nk + 7;
       double n2[6] = {0, 0, 0, 0, 0, 0};
       for (int i = lane; i < p.K; i += 32) {
@@ -1324,15 +1327,33 @@ __global__ void __launch_bounds__(512) policy_kernel(const PolicyArgs p) {
         }
       }
     }
-    __syncthreads();
   }
-  if (!p.do_riccati || warp != 0) return;
+}
+
+__global__ void __launch_bounds__(32) riccati_kernel(const PolicyArgs p) {
+  __shared__ double S[49], SA[49], A[49], Sn[49], bv[7], Sb[7], bS[7], AtSb[7], hh[7];
+  const int lane = threadIdx.x & 31;
   for (int e = lane; e < 49; e += 32) S[e] = (e % 8 == 0) ? p.qf[e / 7] : 0.0;
   if (lane == 0) p.flag[0] = 0;
+  // (A_k, b_k) of the next step are loaded into registers while step k+1 computes:
+  // the recursion is serial, so an L2 round trip per step would sit on its path
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0;
+  {
+    const int k = p.H - 1;
+    a0 = p.a_disc[(size_t)k * 49 + lane];
+    if (lane + 32 < 49) a1 = p.a_disc[(size_t)k * 49 + lane + 32];
+    if (lane < 7) b0 = p.b_disc[(size_t)k * 7 + lane];
+  }
   __syncwarp();
   for (int k = p.H - 1; k >= 0; --k) {
-    for (int e = lane; e < 49; e += 32) A[e] = p.a_disc[(size_t)k * 49 + e];
-    if (lane < 7) bv[lane] = p.b_disc[(size_t)k * 7 + lane];
+    A[lane] = a0;
+    if (lane + 32 < 49) A[lane + 32] = a1;
+    if (lane < 7) bv[lane] = b0;
+    if (k > 0) {
+      a0 = p.a_disc[(size_t)(k - 1) * 49 + lane];
+      if (lane + 32 < 49) a1 = p.a_disc[(size_t)(k - 1) * 49 + lane + 32];
+      if (lane < 7) b0 = p.b_disc[(size_t)(k - 1) * 7 + lane];
+    }
     __syncwarp();
     if (lane < 7) {
       double s1 = 0.0, s2 = 0.0;
