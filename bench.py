@@ -238,6 +238,20 @@ def extras(torch, dev, sc, flat, plan, mp):
         for i in range(3):
             policy.build_policy(nom, fl, cfg.synthesis, eng, np.random.default_rng(i))
         out["policy_build_ms_e2e"] = 1e3 * (time.perf_counter() - t0) / 3
+    # mppi.optimize through the public API on the C4 snapshot (K=4096, H=50, 3
+    # iterations, host buffers in/out): numpy noise drawn on the host (reference
+    # parity; iteration i+1's draw overlaps iteration i) vs device-drawn Philox noise
+    import dataclasses
+    from paper_2509_16079_b200 import mppi as mppi_mod
+    mcfg = dataclasses.replace(cfg.mppi, batch=K_SAMPLES, input_stdev=SIGMA, temperature=LAMBDA)
+    warm = np.full(HORIZON, -6.0)
+    for name, mk in (("numpy_rng", lambda i: np.random.default_rng(i)),
+                     ("device_noise", lambda i: mppi_mod.DeviceNoise(i))):
+        mppi_mod.optimize(sc["x0"], fl, warm, mcfg, eng, mk(0), iterations=3)
+        t0 = time.perf_counter()
+        for i in range(3):
+            mppi_mod.optimize(sc["x0"], fl, warm, mcfg, eng, mk(1 + i), iterations=3)
+        out[f"optimize_c4_3iter_ms_{name}"] = 1e3 * (time.perf_counter() - t0) / 3
     plan.set_fluid(flat)
     # one full replanning cycle at the paper's operating point (nmpc.replan: 10-step
     # projection, 3 MPPI iterations K=256 over the 67-step tail, nominal, policy; cap 60)

@@ -175,6 +175,15 @@ int vpm_mppi_partial(vpm_plan *p, const double *d_cost, int rows, int row_begin,
 int vpm_mppi_combine(const double *d_partials, int W, int T, double temperature,
                      double *d_ustar, int32_t *d_flag, void *stream);
 
+/* Performance mode (no reference counterpart): standard-normal
+ * noise drawn on the device for rows [row_begin, row_begin + rows) of one
+ * iteration's (K, T) noise matrix -- counter-based Philox4x32-10 keyed by seed,
+ * subsequence = global noise row, offset fixed by iteration, so any sharding of the
+ * rows draws the same numbers.  d_out: (rows, T) FP64.  The reference-parity path
+ * keeps host-drawn numpy noise (mppi.py:42). */
+int vpm_noise_philox(uint64_t seed, uint64_t iteration, int row_begin, int rows, int T,
+                     double *d_out, void *stream);
+
 /* Whole MPPI iteration on one device (batch + partial + combine), optionally
  * replayed from a CUDA graph captured on first use (use_graph != 0).
  * d_noise: (B_total - 1, T).  d_cost scratch (B_total) and d_partial (T+2). */

@@ -114,6 +114,7 @@ def lib():
             "vpm_mppi_partial": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, C.c_double, C.c_int,
                                            C.c_double, vp, vp]),
             "vpm_mppi_combine": (C.c_int, [vp, C.c_int, C.c_int, C.c_double, vp, vp, vp]),
+            "vpm_noise_philox": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, vp, vp]),
             "vpm_mppi_iteration": (C.c_int, [vp, vp, vp, vp, C.c_double, C.c_int, C.c_int,
                                              C.c_double, vp, vp, vp, vp, vp, C.c_int, vp]),
             "vpm_mppi_optimize_host": (C.c_int, [vp, _D, _D, _D, C.c_int, C.c_int, C.c_int,
@@ -147,7 +148,7 @@ def lib():
 
 EXPORTED = ("vpm_step", "vpm_rollout", "vpm_batch_rollout", "vpm_batch_rollout_x0", "vpm_threads",
             "vpm_last_error", "vpm_plan_create", "vpm_plan_destroy", "vpm_plan_set_fluid",
-            "vpm_plan_batch", "vpm_mppi_partial", "vpm_mppi_combine", "vpm_mppi_iteration",
+            "vpm_plan_batch", "vpm_mppi_partial", "vpm_mppi_combine", "vpm_noise_philox", "vpm_mppi_iteration",
             "vpm_mppi_optimize_host", "vpm_plan_timing", "vpm_fp32_peak_probe", "vpm_launch_shape",
             "vpm_boundary_inverse", "vpm_policy_fit", "vpm_build_policy_host",
             "vpm_policy_fit_host", "vpm_tvlqr_host", "vpm_plan_project", "vpm_plan_cloud",

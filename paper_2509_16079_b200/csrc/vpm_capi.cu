@@ -626,6 +626,19 @@ int vpm_mppi_combine(const double *d_partials, int W, int T, double temperature,
   return VPM_OK;
 }
 
+int vpm_noise_philox(uint64_t seed, uint64_t iteration, int row_begin, int rows, int T, double *d_out,
+                     void *stream) {
+  if (row_begin < 0 || rows < 0 || T < 0) return fail_cfg("bad noise shape");
+  if (rows == 0 || T == 0) return VPM_OK;
+  if (!d_out) return fail_cfg("noise output must not be null");
+  const long long n = (long long)rows * ((T + 1) / 2);
+  const int bs = 256;
+  vpm::noise_philox_kernel<<<(unsigned)((n + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>(
+      (unsigned long long)seed, (unsigned long long)iteration, row_begin, rows, T, d_out);
+  CK(cudaGetLastError());
+  return VPM_OK;
+}
+
 int vpm_mppi_iteration(vpm_plan *p, const double *d_x0, double *d_ustar, const double *d_noise,
                        double sigma, int B_total, int T, double temperature, const double *d_q,
                        const double *d_xperch, double *d_cost, double *d_partial, int32_t *d_flag,

@@ -54,6 +54,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <curand_kernel.h>
 #include <math.h>
 #include <stdint.h>
 
@@ -1177,6 +1178,28 @@ __global__ void mppi_combine_kernel(const double *__restrict__ parts, int W, int
     ustar[t] = S / Z;
   }
   if (threadIdx.x == 0 && flag) *flag = 0;
+}
+
+// ---- device noise (performance mode) ----------------------------------
+// Standard normals for rows [row_begin, row_begin + rows) of one iteration's (K, T)
+// MPPI noise matrix.  One thread per (row, pair of steps): counter-based
+// Philox4x32-10 keyed by seed, subsequence = global noise row, offset = the
+// iteration's block of 4 ceil(T/2) draws + 4 per pair, Box-Muller in FP64
+// (curand_normal2_double).  The value at (g, t) depends only on (seed, iteration,
+// g, t), so every sharding of the rows draws the same numbers; writes coalesce.
+__global__ void noise_philox_kernel(unsigned long long seed, unsigned long long iteration,
+                                    int row_begin, int rows, int T, double *__restrict__ out) {
+  const int P = (T + 1) >> 1;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)rows * P) return;
+  const int r = (int)(idx / P), pr = (int)(idx - (long long)r * P);
+  curandStatePhilox4_32_10_t st;
+  curand_init(seed, (unsigned long long)(row_begin + r),
+              iteration * 4ull * (unsigned long long)P + 4ull * (unsigned long long)pr, &st);
+  const double2 v = curand_normal2_double(&st);
+  double *o = out + (size_t)r * T + 2 * pr;
+  o[0] = v.x;
+  if (2 * pr + 1 < T) o[1] = v.y;
 }
 
 // ---- sample-built TVLQR tracking controller (policy.py:121-233) ----------------------

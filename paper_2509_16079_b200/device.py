@@ -189,6 +189,16 @@ def mppi_combine(partials, temperature: float, ustar, flag=None, stream=None):
                                       _p(flag), _stream(stream)), "mppi_combine")
 
 
+def noise_philox(seed: int, iteration: int, out, row_begin: int = 0, stream=None):
+    """Fill the CUDA float64 tensor ``out`` (rows, T) with rows [row_begin, row_begin
+    + rows) of iteration ``iteration``'s device-drawn standard-normal noise
+    (``vpm_noise_philox``: counter-based Philox keyed by (seed, iteration, row))."""
+    rows, T = int(out.shape[0]), int(out.shape[1])
+    check(_lib.lib().vpm_noise_philox(int(seed) & (2**64 - 1), int(iteration), int(row_begin), rows, T,
+                                      _p(out), _stream(stream)), "noise_philox")
+    return out
+
+
 def policy_fit(nom_x, nom_u, cloud_x, cloud_u, status, dt: float, q_running, r_running: float,
                q_final, stream=None):
     """Device regression + Riccati (policy.py:121-233) on device tensors; returns

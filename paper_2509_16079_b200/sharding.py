@@ -80,6 +80,15 @@ class ShardedMppi:
     def set_noise(self, noise_rows):
         self.noise = noise_rows
 
+    def draw_noise(self, seed: int, iteration: int, stream=None):
+        """Performance mode: draw this rank's noise rows on the device (Philox keyed
+        by (seed, iteration, global row), so the union over ranks is the same matrix
+        for any world size) into the global-row-indexed noise buffer."""
+        from .device import noise_philox
+        lo, hi = max(self.begin - 1, 0), self.end - 1  # noise row of global row g is g - 1
+        if hi > lo:
+            noise_philox(seed, iteration, self.noise[lo:hi], row_begin=lo, stream=stream)
+
     def iteration(self, stream=None) -> None:
         from .device import mppi_combine
         rows = self.end - self.begin

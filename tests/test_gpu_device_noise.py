@@ -1,0 +1,85 @@
+"""Performance-mode noise drawn on the device (vpm_noise_philox).
+
+Not a reference-parity path (the reference draws numpy PCG64 normals, mppi.py:42);
+what is checked: the draws are standard normal, deterministic, independent of how
+the rows are sharded, and mppi.optimize(..., rng=DeviceNoise(seed)) is bitwise the
+host-noise pipeline fed with the same numbers."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    torch.cuda.set_device(0)
+    return torch
+
+
+def test_philox_noise_is_standard_normal_and_shard_independent(torch_cuda):
+    torch = torch_cuda
+    from paper_2509_16079_b200.device import noise_philox
+    from paper_2509_16079_b200.sharding import ShardedMppi, row_range
+    K, H = 4096, 50
+    full = noise_philox(11, 0, torch.empty((K, H), dtype=torch.float64, device="cuda"))
+    again = noise_philox(11, 0, torch.empty((K, H), dtype=torch.float64, device="cuda"))
+    nxt = noise_philox(11, 1, torch.empty((K, H), dtype=torch.float64, device="cuda"))
+    a = full.cpu().numpy()
+    assert np.array_equal(a, again.cpu().numpy())
+    assert abs(a.mean()) < 0.01 and abs(a.std() - 1.0) < 0.01
+    assert abs(np.mean(a ** 4) - 3.0) < 0.05                   # Gaussian kurtosis
+    assert abs(np.corrcoef(a[:, :-1].ravel(), a[:, 1:].ravel())[0, 1]) < 0.01
+    assert not np.allclose(a, nxt.cpu().numpy())
+    # odd horizon and a row slice drawn on its own equal the full draw
+    odd = noise_philox(11, 0, torch.empty((K, 49), dtype=torch.float64, device="cuda")).cpu().numpy()
+    assert np.isfinite(odd).all()
+    part = noise_philox(11, 0, torch.empty((500, H), dtype=torch.float64, device="cuda"), row_begin=1000)
+    assert np.array_equal(part.cpu().numpy(), a[1000:1500])
+    # ShardedMppi.draw_noise: every rank fills its rows; the union is the W = 1 matrix
+    union = torch.zeros((K, H), dtype=torch.float64, device="cuda")
+    for r in range(3):
+        sh = ShardedMppi.__new__(ShardedMppi)
+        sh.begin, sh.end = row_range(K + 1, 3, r)
+        sh.noise = union
+        sh.draw_noise(11, 0)
+    assert np.array_equal(union.cpu().numpy(), a)
+
+
+class _Replay:
+    """A numpy-Generator stand-in that returns pre-drawn blocks from normal()."""
+
+    class _BG:
+        state = None
+
+    def __init__(self, blocks):
+        self.blocks = list(blocks)
+        self.bit_generator = self._BG()
+
+    def normal(self, loc, scale, size):
+        return self.blocks.pop(0)
+
+
+def test_optimize_with_device_noise_equals_host_pipeline(torch_cuda):
+    torch = torch_cuda
+    from paper_2509_16079_b200 import config, mppi, rollout, vpm
+    from paper_2509_16079_b200.device import noise_philox
+    cfg = config.ExperimentConfig()
+    eng = rollout.Engine.from_config(cfg)
+    x0 = np.asarray(cfg.scenario.x0, float)
+    fl = vpm.inject_ring(vpm.FluidState.empty(cfg.vpm),
+                         vpm.RingDisturbance.from_speed([1.0, -0.1], 7.5, 0.28, 0.02, -1.0))
+    warm = np.full(cfg.mppi.horizon, -6.0)
+    dn = mppi.DeviceNoise(5)
+    u_dev = mppi.optimize(x0, fl, warm, cfg.mppi, eng, dn, iterations=3)
+    assert dn.iteration == 3
+    K, H = cfg.mppi.batch, cfg.mppi.horizon
+    blocks = [noise_philox(5, i, torch.empty((K, H), dtype=torch.float64, device="cuda")).cpu().numpy()
+              for i in range(3)]
+    u_host = mppi.optimize(x0, fl, warm, cfg.mppi, eng, _Replay(blocks), iterations=3)
+    np.testing.assert_array_equal(u_dev, u_host)
+    # the next call continues the stream (iterations 3, 4) and stays deterministic
+    u2 = mppi.optimize(x0, fl, warm, cfg.mppi, eng, mppi.DeviceNoise(5, iteration=3), iterations=2)
+    u3 = mppi.optimize(x0, fl, warm, cfg.mppi, eng, dn, iterations=2)
+    np.testing.assert_array_equal(u2, u3)
