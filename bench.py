@@ -346,9 +346,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional-test hooks (never set by the driver): every rank on device 0 and
+    # gloo instead of NCCL, to exercise the multi-rank code path on a 1-GPU box
+    if os.environ.get("VPM_BENCH_ONE_DEVICE"):
+        local = 0
+    backend = os.environ.get("VPM_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2509_16079_b200 import _lib
     from paper_2509_16079_b200.device import DevicePlan, fp32_peak_gflops, launch_shape
     from paper_2509_16079_b200.sharding import ShardedMppi
