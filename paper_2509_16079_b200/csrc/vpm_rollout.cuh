@@ -1063,8 +1063,10 @@ constexpr int PCH_WARPS = 8, PCH_ROWS = 8 * PCH_WARPS;  // 256 threads, 64 rows 
 __global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
     const double *__restrict__ cost, int rows, int row_begin, const double *__restrict__ ustar,
     const double *__restrict__ noise, double sigma, double ulim, int T, double lambda,
-    double *__restrict__ chunks, unsigned *__restrict__ ticket, double *__restrict__ part) {
-  extern __shared__ double sh[];  // [PCH_WARPS][T] control sums, 2 PCH_WARPS, [G] scales
+    double *__restrict__ chunks, unsigned *__restrict__ ticket, double *__restrict__ part, int CT) {
+  // [PCH_WARPS][T] control sums | 2 PCH_WARPS + PCH_WARPS reductions | [CT][T+2] chunk
+  // tile | [CT] chunk scales | [T] running S (last CTA)
+  extern __shared__ double sh[];
   double *sacc = sh, *sred = sh + PCH_WARPS * T;
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1132,26 +1134,44 @@ __global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
   __threadfence();
   const int G = gridDim.x;
   const volatile double *vc = chunks;  // written by other SMs: bypass L1
-  double *scale = sred + 2 * PCH_WARPS;  // [G]
+  double *tile = sred + 3 * PCH_WARPS, *stile = tile + (size_t)CT * ld, *sS = stile + CT;
+  // global minimum: all chunk minima loaded in parallel (min is exact, order-free)
   double gm = INFINITY;
-  for (int c = 0; c < G; ++c) gm = fmin(gm, vc[(size_t)c * ld]);
-  for (int c = threadIdx.x; c < G; c += blockDim.x) {
-    const double jc = vc[(size_t)c * ld];
-    scale[c] = (isfinite(gm) && isfinite(jc)) ? exp(-(jc - gm) / lambda) : 0.0;
-  }
+  for (int c = threadIdx.x; c < G; c += blockDim.x) gm = fmin(gm, vc[(size_t)c * ld]);
+  for (int o = 16; o >= 1; o >>= 1) gm = fmin(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+  if (lane == 0) sred[2 * PCH_WARPS + warp] = gm;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) sS[t] = 0.0;
   __syncthreads();
+  gm = INFINITY;
+  for (int w = 0; w < PCH_WARPS; ++w) gm = fmin(gm, sred[2 * PCH_WARPS + w]);
+  // Z and S summed over the chunks in chunk order, CT chunks at a time staged in
+  // shared memory by all threads (coalesced: the chunk rows are contiguous) -- the
+  // serial part reads shared memory only
+  double Z = 0.0;
+  for (int c0 = 0; c0 < G; c0 += CT) {
+    const int nc = min(CT, G - c0);
+    for (int e = threadIdx.x; e < nc * ld; e += blockDim.x) tile[e] = vc[(size_t)c0 * ld + e];
+    __syncthreads();
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+      const double jc = tile[c * ld];
+      stile[c] = (isfinite(gm) && isfinite(jc)) ? exp(-(jc - gm) / lambda) : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int c = 0; c < nc; ++c) Z += tile[c * ld + 1] * stile[c];
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+      double S = sS[t];
+      for (int c = 0; c < nc; ++c) S += tile[c * ld + 2 + t] * stile[c];
+      sS[t] = S;
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
-    double Z = 0.0;
-    for (int c = 0; c < G; ++c) Z += vc[(size_t)c * ld + 1] * scale[c];
     part[0] = gm;
     part[1] = Z;
     *ticket = 0u;
   }
-  for (int t = threadIdx.x; t < T; t += blockDim.x) {
-    double S = 0.0;
-    for (int c = 0; c < G; ++c) S += vc[(size_t)c * ld + 2 + t] * scale[c];
-    part[2 + t] = S;
-  }
+  for (int t = threadIdx.x; t < T; t += blockDim.x) part[2 + t] = sS[t];
 }
 
 // Combine W gathered partials in rank order.
