@@ -607,15 +607,13 @@ int vpm_mppi_partial(vpm_plan *p, const double *d_cost, int rows, int row_begin,
     CK(cudaMalloc(&p->d_ticket, sizeof(unsigned)));
     CK(cudaMemset(p->d_ticket, 0, sizeof(unsigned)));
   }
-  const int CT = std::max(1, std::min(64, 4096 / (T + 2)));  // chunks staged per tile
-  const size_t smem = sizeof(double) * ((size_t)vpm::PCH_WARPS * T + 3 * vpm::PCH_WARPS +
-                                        (size_t)CT * (T + 2) + CT + T);
+  const size_t smem = sizeof(double) * ((size_t)vpm::PCH_WARPS * (T + 1) + 3 * vpm::PCH_WARPS);
   if (smem > 48 * 1024)
     CK(cudaFuncSetAttribute(vpm::mppi_partial_chunked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
   vpm::mppi_partial_chunked_kernel<<<G, 32 * vpm::PCH_WARPS, smem, (cudaStream_t)stream>>>(
       d_cost, rows, row_begin, d_ustar, d_noise, sigma, p->P.u_lim, T, temperature, p->d_wbuf, p->d_ticket,
-      d_partial, CT);
+      d_partial);
   CK(cudaGetLastError());
   return VPM_OK;
 }

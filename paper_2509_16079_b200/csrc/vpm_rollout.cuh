@@ -1063,11 +1063,11 @@ constexpr int PCH_WARPS = 8, PCH_ROWS = 8 * PCH_WARPS;  // 256 threads, 64 rows 
 __global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
     const double *__restrict__ cost, int rows, int row_begin, const double *__restrict__ ustar,
     const double *__restrict__ noise, double sigma, double ulim, int T, double lambda,
-    double *__restrict__ chunks, unsigned *__restrict__ ticket, double *__restrict__ part, int CT) {
-  // [PCH_WARPS][T] control sums | 2 PCH_WARPS + PCH_WARPS reductions | [CT][T+2] chunk
-  // tile | [CT] chunk scales | [T] running S (last CTA)
+    double *__restrict__ chunks, unsigned *__restrict__ ticket, double *__restrict__ part) {
+  // [PCH_WARPS][T+1] control sums (then the last CTA's group sums) | 3 PCH_WARPS
+  // reductions
   extern __shared__ double sh[];
-  double *sacc = sh, *sred = sh + PCH_WARPS * T;
+  double *sacc = sh, *sred = sh + PCH_WARPS * (T + 1);
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ld = T + 2;
@@ -1133,45 +1133,56 @@ __global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
   if (!s_last) return;
   __threadfence();
   const int G = gridDim.x;
-  const volatile double *vc = chunks;  // written by other SMs: bypass L1
-  double *tile = sred + 3 * PCH_WARPS, *stile = tile + (size_t)CT * ld, *sS = stile + CT;
+  // chunk records were written by other SMs: read them through L2 (__ldcg)
   // global minimum: all chunk minima loaded in parallel (min is exact, order-free)
   double gm = INFINITY;
-  for (int c = threadIdx.x; c < G; c += blockDim.x) gm = fmin(gm, vc[(size_t)c * ld]);
+  for (int c = threadIdx.x; c < G; c += blockDim.x) gm = fmin(gm, __ldcg(chunks + (size_t)c * ld));
   for (int o = 16; o >= 1; o >>= 1) gm = fmin(gm, __shfl_xor_sync(0xffffffffu, gm, o));
   if (lane == 0) sred[2 * PCH_WARPS + warp] = gm;
-  for (int t = threadIdx.x; t < T; t += blockDim.x) sS[t] = 0.0;
   __syncthreads();
   gm = INFINITY;
   for (int w = 0; w < PCH_WARPS; ++w) gm = fmin(gm, sred[2 * PCH_WARPS + w]);
-  // Z and S summed over the chunks in chunk order, CT chunks at a time staged in
-  // shared memory by all threads (coalesced: the chunk rows are contiguous) -- the
-  // serial part reads shared memory only
-  double Z = 0.0;
-  for (int c0 = 0; c0 < G; c0 += CT) {
-    const int nc = min(CT, G - c0);
-    for (int e = threadIdx.x; e < nc * ld; e += blockDim.x) tile[e] = vc[(size_t)c0 * ld + e];
-    __syncthreads();
-    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
-      const double jc = tile[c * ld];
-      stile[c] = (isfinite(gm) && isfinite(jc)) ? exp(-(jc - gm) / lambda) : 0.0;
+  // Z and S in a fixed two-level order: warp w sums the contiguous chunk group
+  // [w G / PCH_WARPS, (w+1) G / PCH_WARPS) in chunk order (lanes over the T+1
+  // columns {Z, S_0..S_T-1}, coalesced chunk-row loads), then the group sums are
+  // added in group order.  The order depends only on G.
+  double *gsum = sacc;  // [PCH_WARPS][T+1], the chunk's control sums are no longer needed
+  const int c_lo = (int)((long long)warp * G / PCH_WARPS), c_hi = (int)((long long)(warp + 1) * G / PCH_WARPS);
+  for (int col0 = 0; col0 < T + 1; col0 += 32) {
+    const int col = col0 + lane;
+    double acc = 0.0;
+    int c = c_lo;
+    for (; c + 4 <= c_hi; c += 4) {  // four chunk rows in flight per lane
+      double v[4], jc[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        jc[q] = __ldcg(chunks + (size_t)(c + q) * ld);
+        v[q] = col <= T ? __ldcg(chunks + (size_t)(c + q) * ld + 1 + col) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double sc = (isfinite(gm) && isfinite(jc[q])) ? exp(-(jc[q] - gm) / lambda) : 0.0;
+        acc += v[q] * sc;
+      }
     }
-    __syncthreads();
-    if (threadIdx.x == 0)
-      for (int c = 0; c < nc; ++c) Z += tile[c * ld + 1] * stile[c];
-    for (int t = threadIdx.x; t < T; t += blockDim.x) {
-      double S = sS[t];
-      for (int c = 0; c < nc; ++c) S += tile[c * ld + 2 + t] * stile[c];
-      sS[t] = S;
+    for (; c < c_hi; ++c) {
+      const double jc = __ldcg(chunks + (size_t)c * ld);
+      const double v = col <= T ? __ldcg(chunks + (size_t)c * ld + 1 + col) : 0.0;
+      const double sc = (isfinite(gm) && isfinite(jc)) ? exp(-(jc - gm) / lambda) : 0.0;
+      acc += v * sc;
     }
-    __syncthreads();
+    if (col <= T) gsum[warp * (T + 1) + col] = acc;
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < T + 1; col += blockDim.x) {
+    double tot = 0.0;
+    for (int w = 0; w < PCH_WARPS; ++w) tot += gsum[w * (T + 1) + col];
+    part[1 + col] = tot;  // part[1] = Z, part[2 + t] = S_t
   }
   if (threadIdx.x == 0) {
     part[0] = gm;
-    part[1] = Z;
     *ticket = 0u;
   }
-  for (int t = threadIdx.x; t < T; t += blockDim.x) part[2 + t] = sS[t];
 }
 
 // Combine W gathered partials in rank order.
