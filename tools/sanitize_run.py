@@ -42,3 +42,7 @@ new = replan.replan(replan.ReplanRequest(x=x, fluid=fl, policy=pol, t=0.0, t_pro
                     np.random.default_rng(2))
 print("replan", new is not None)
 print("induced", vpm.induced_velocity_at([[0.1, 0.2]], fl.wake_pos[:fl.n_wake], fl.wake_gamma[:fl.n_wake], r_core=0.02))
+# device-noise optimiser (noise kernel + MPPI partial / combine)
+u2 = mppi.optimize(x, fl, np.full(12, -6.0), cfg.mppi, eng, mppi.DeviceNoise(4), iterations=2)
+torch.cuda.synchronize()
+print("device noise ok", np.isfinite(u2).all())
