@@ -99,35 +99,51 @@ def _replan_locked(torch, plan, dev, f64, req, cfg, engine, rng):
     if len(tail) == 0:
         return None  # nothing to re-plan; the reference draws nothing on this path either
     plan.set_fluid(req.fluid)
-    # 1. closed-loop projection; its wake becomes the plan's snapshot on the device
-    pstat, xdev = plan.project(f64(req.x), int(req.t_proj), f64(req.policy.gains), f64(old.states),
-                               f64(old.inputs), old.t_start, float(req.t), write_snapshot=True)
-    x0 = xdev[0]
     mc, sc = cfg.mppi, cfg.synthesis
     H, K, iters, k = len(tail), int(mc.batch), int(mc.iterations), int(sc.n_samples)
     run_mppi = bool(H and iters and K)
+    # Every small input goes up in ONE non-blocking copy from the pinned staging
+    # buffer: a torch.as_tensor of a pageable numpy array would synchronise the
+    # stream and stall the host behind the launches already queued.
+    gains = np.asarray(req.policy.gains, dtype=float)
+    states = np.asarray(old.states, dtype=float)
+    inputs = np.asarray(old.inputs, dtype=float)
+    parts = [np.clip(np.asarray(tail, dtype=float), -lim, lim), np.asarray(req.x, dtype=float), gains,
+             states, inputs, np.asarray(mc.q_terminal, dtype=float), np.asarray(mc.x_perch, dtype=float),
+             np.asarray(sc.state_stdev, dtype=float), np.asarray(sc.q_running, dtype=float),
+             np.asarray(sc.q_final, dtype=float)]
+    offs = np.cumsum([0] + [a.size for a in parts])
+    nh = int(offs[-1])
+    n_it = K * H if run_mppi else 0
+    n_cloud = (k + 1) * 7 + (k + 1) * H
+    host = plan.staging(nh + iters * n_it + n_cloud)
+    hv = host.numpy()
+    for a, o in zip(parts, offs[:-1]):
+        hv[o:o + a.size] = a.ravel()
+    head = host[:nh].to(dev, non_blocking=True)
+    seg = [head[offs[i]:offs[i + 1]] for i in range(len(parts))]
+    u = seg[0]  # u* (updated in place by the MPPI iterations)
+    d_x, d_gains, d_states, d_inputs = seg[1], seg[2].view(gains.shape), seg[3].view(states.shape), seg[4]
+    q, xp, d_sx, d_qr, d_qf = seg[5], seg[6], seg[7], seg[8], seg[9]
+    # 1. closed-loop projection; its wake becomes the plan's snapshot on the device
+    pstat, xdev = plan.project(d_x, int(req.t_proj), d_gains, d_states, d_inputs, old.t_start,
+                               float(req.t), write_snapshot=True)
+    x0 = xdev[0]
     # 2./3. the success path's draws and the MPPI iterations (mppi.py:62-84),
     # pipelined: each iteration's noise is drawn on the host and copied while the
     # device runs the previous launch; one failure flag per iteration
     saved = rng.bit_generator.state
-    n_it = K * H if run_mppi else 0
-    n_cloud = (k + 1) * 7 + (k + 1) * H
-    host = plan.staging(H + iters * n_it + n_cloud)
-    hv = host.numpy()
-    hv[:H] = np.clip(np.asarray(tail, dtype=float), -lim, lim)
-    u = host[:H].to(dev, non_blocking=True)
     flags = torch.zeros(max(iters, 1), dtype=torch.int32, device=dev)
     if run_mppi:
         scratch = {"cost": torch.empty(K + 1, dtype=torch.float64, device=dev),
                    "partial": torch.empty(H + 2, dtype=torch.float64, device=dev)}
-        q, xp = f64(mc.q_terminal), f64(mc.x_perch)
         for i in range(iters):
-            lo = H + i * n_it
+            lo = nh + i * n_it
             hv[lo:lo + n_it] = rng.normal(0.0, 1.0, (K, H)).ravel()
             d_noise = host[lo:lo + n_it].to(dev, non_blocking=True).view(K, H)
             scratch["flag"] = flags[i:i + 1]
             plan.mppi_iteration(x0, u, d_noise, mc.input_stdev, K + 1, mc.temperature, q, xp, scratch)
-    lo = H + iters * n_it
+    lo = nh + iters * n_it
     dx0 = rng.normal(0.0, 1.0, (k, 7))
     du = rng.normal(0.0, 1.0, (k, H))
     cx = hv[lo:lo + (k + 1) * 7].reshape(k + 1, 7)
@@ -138,12 +154,12 @@ def _replan_locked(torch, plan, dev, f64, req, cfg, engine, rng):
     d_cx = dcl[:(k + 1) * 7].view(k + 1, 7)
     d_cu = dcl[(k + 1) * 7:].view(k + 1, H)
     # 4. nominal (row 0) + perturbed cloud (rows 1..k) in one launch (policy.py:66-91)
-    cstat, ctraj = plan.cloud(x0, d_cx, f64(sc.state_stdev), u, d_cu, sc.input_stdev)
+    cstat, ctraj = plan.cloud(x0, d_cx, d_sx, u, d_cu, sc.input_stdev)
     traj = ctraj[0]
     cu_dev = torch.clamp(u.view(1, H) + d_cu[1:] * sc.input_stdev, -lim, lim)
     # 5. regression + Riccati around the nominal (policy.py:247-266)
-    _, _, _, _, gains, fflag = policy_fit(traj, u, ctraj[1:], cu_dev, cstat[1:], dt, f64(sc.q_running),
-                                          sc.r_running, f64(sc.q_final))
+    _, _, _, _, d_gain, fflag = policy_fit(traj, u, ctraj[1:], cu_dev, cstat[1:], dt, d_qr, sc.r_running,
+                                           d_qf)
     # 6. the one synchronisation: every decision the reference makes, in its order
     ints = torch.cat([pstat.view(1), flags.to(torch.int64), cstat, fflag[:1].to(torch.int64)]).cpu().numpy()
     if ints[0] != 0:
@@ -163,7 +179,7 @@ def _replan_locked(torch, plan, dev, f64, req, cfg, engine, rng):
     if int((st[1:] == 0).sum()) < 6 or ints[-1] != 0:
         return None  # RankDeficientData / FloatingPointError after all draws
     nominal = NominalTrajectory(states=traj.cpu().numpy(), inputs=u.cpu().numpy(), dt=dt, t_start=t_new)
-    return Policy(gains=gains.cpu().numpy(), nominal=nominal, q_final=np.asarray(sc.q_final, dtype=float))
+    return Policy(gains=d_gain.cpu().numpy(), nominal=nominal, q_final=np.asarray(sc.q_final, dtype=float))
 
 
 def bootstrap_policy(cfg: ExperimentConfig, engine: Engine, rng: np.random.Generator) -> Policy:
