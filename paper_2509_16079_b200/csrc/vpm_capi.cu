@@ -313,6 +313,9 @@ struct vpm_plan {
   double *d_plev = nullptr;
   int n_wake = 0, ring_a = -1, ring_b = -1, n_prev = 0;
   double prev_lev = 0.0;
+  double *d_snap = nullptr;  // the snapshot arrays above, one block
+  double *h_snap = nullptr;  // pinned host mirror of d_snap (set_fluid staging)
+  size_t snap_doubles = 0;
   double *d_wbuf = nullptr;  // chunk partials of the MPPI softmax reduction
   size_t wbuf_len = 0;
   unsigned *d_ticket = nullptr;  // last-CTA ticket of the chunked reduction (re-armed by it)
@@ -401,15 +404,26 @@ vpm_plan *vpm_plan_create(const int64_t *iparams, const double *fparams, int max
   p->max_rows = max_rows;
   p->H = H;
   const int cap4 = P.cap + 4;
+  // The snapshot lives in ONE device block with a pinned host mirror, so
+  // vpm_plan_set_fluid uploads it with a single copy:
+  //   wpos 2 cap4 | wgam cap4 | wage cap4 (int64) | ppos 2 nb | pgam nb | ema nb |
+  //   plev 1 | scal 4 int32 (2 doubles)
+  p->snap_doubles = (size_t)4 * cap4 + 4 * P.nb + 3;
   bool ok = cudaMalloc(&p->d_ainv, inv.size() * sizeof(double)) == cudaSuccess &&
-            cudaMalloc(&p->d_wpos, sizeof(double) * 2 * cap4) == cudaSuccess &&
-            cudaMalloc(&p->d_wgam, sizeof(double) * cap4) == cudaSuccess &&
-            cudaMalloc(&p->d_wage, sizeof(int64_t) * cap4) == cudaSuccess &&
-            cudaMalloc(&p->d_ppos, sizeof(double) * 2 * P.nb) == cudaSuccess &&
-            cudaMalloc(&p->d_pgam, sizeof(double) * P.nb) == cudaSuccess &&
-            cudaMalloc(&p->d_ema, sizeof(double) * P.nb) == cudaSuccess &&
-            cudaMalloc(&p->d_scal, sizeof(int32_t) * 4) == cudaSuccess &&
-            cudaMalloc(&p->d_plev, sizeof(double)) == cudaSuccess;
+            cudaMalloc(&p->d_snap, sizeof(double) * p->snap_doubles) == cudaSuccess &&
+            cudaHostAlloc(&p->h_snap, sizeof(double) * p->snap_doubles, cudaHostAllocDefault) == cudaSuccess;
+  if (ok) {
+    double *b = p->d_snap;
+    p->d_wpos = b;
+    p->d_wgam = b + 2 * cap4;
+    p->d_wage = reinterpret_cast<int64_t *>(b + 3 * cap4);
+    p->d_ppos = b + 4 * cap4;
+    p->d_pgam = p->d_ppos + 2 * P.nb;
+    p->d_ema = p->d_pgam + P.nb;
+    p->d_plev = p->d_ema + P.nb;
+    p->d_scal = reinterpret_cast<int32_t *>(p->d_plev + 1);
+    std::memset(p->h_snap, 0, sizeof(double) * p->snap_doubles);
+  }
   if (ok) {
     const int32_t empty[4] = {0, -1, -1, 0};
     ok = cudaMemcpy(p->d_scal, empty, sizeof(empty), cudaMemcpyHostToDevice) == cudaSuccess &&
@@ -429,14 +443,8 @@ void vpm_plan_destroy(vpm_plan *p) {
   if (!p) return;
   cudaSetDevice(p->device);
   cudaFree(p->d_ainv);
-  cudaFree(p->d_wpos);
-  cudaFree(p->d_wgam);
-  cudaFree(p->d_wage);
-  cudaFree(p->d_ppos);
-  cudaFree(p->d_pgam);
-  cudaFree(p->d_ema);
-  cudaFree(p->d_scal);
-  cudaFree(p->d_plev);
+  cudaFree(p->d_snap);
+  if (p->h_snap) cudaFreeHost(p->h_snap);
   cudaFree(p->d_wbuf);
   cudaFree(p->d_ticket);
   cudaFree(p->hscratch);
@@ -451,24 +459,28 @@ int vpm_plan_set_fluid(vpm_plan *p, const vpm_fluid *f) {
   if (rc) return rc;
   CK(cudaSetDevice(p->device));
   CK(cudaDeviceSynchronize());  // no launch of any stream may still read the old snapshot
+  // pack the used parts into the pinned mirror at their device offsets, one copy up
+  const int cap4 = p->P.cap + 4, nb = p->P.nb;
+  double *h = p->h_snap;
   if (f->n_wake > 0) {
-    CK(cudaMemcpy(p->d_wpos, f->wake_pos, sizeof(double) * 2 * f->n_wake, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(p->d_wgam, f->wake_gamma, sizeof(double) * f->n_wake, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(p->d_wage, f->wake_age, sizeof(int64_t) * f->n_wake, cudaMemcpyHostToDevice));
+    std::memcpy(h, f->wake_pos, sizeof(double) * 2 * f->n_wake);
+    std::memcpy(h + 2 * cap4, f->wake_gamma, sizeof(double) * f->n_wake);
+    std::memcpy(h + 3 * cap4, f->wake_age, sizeof(int64_t) * f->n_wake);
   }
   if (f->n_prev > 0) {
-    CK(cudaMemcpy(p->d_ppos, f->prev_pos, sizeof(double) * 2 * f->n_prev, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(p->d_pgam, f->prev_gamma, sizeof(double) * f->n_prev, cudaMemcpyHostToDevice));
+    std::memcpy(h + 4 * cap4, f->prev_pos, sizeof(double) * 2 * f->n_prev);
+    std::memcpy(h + 4 * cap4 + 2 * nb, f->prev_gamma, sizeof(double) * f->n_prev);
   }
-  CK(cudaMemcpy(p->d_ema, f->ema, sizeof(double) * p->P.nb, cudaMemcpyHostToDevice));
+  std::memcpy(h + 4 * cap4 + 3 * nb, f->ema, sizeof(double) * nb);
+  h[4 * cap4 + 4 * nb] = f->prev_lev;
+  const int32_t scal[4] = {f->n_wake, f->ring_a, f->ring_b, f->n_prev};
+  std::memcpy(h + 4 * cap4 + 4 * nb + 1, scal, sizeof(scal));
+  CK(cudaMemcpy(p->d_snap, h, sizeof(double) * p->snap_doubles, cudaMemcpyHostToDevice));
   p->n_wake = f->n_wake;
   p->ring_a = f->ring_a;
   p->ring_b = f->ring_b;
   p->n_prev = f->n_prev;
   p->prev_lev = f->prev_lev;
-  const int32_t scal[4] = {f->n_wake, f->ring_a, f->ring_b, f->n_prev};
-  CK(cudaMemcpy(p->d_scal, scal, sizeof(scal), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(p->d_plev, &f->prev_lev, sizeof(double), cudaMemcpyHostToDevice));
   return VPM_OK;
 }
 
