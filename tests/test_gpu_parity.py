@@ -174,6 +174,47 @@ def test_device_batch_vs_oracle_margin_aware(torch_cuda, oracle_core, name, K, s
     assert not (differ & clean).any()
 
 
+@pytest.mark.parametrize("name,K,seed", [("scenario_C3.npz", 1024, 31), ("scenario_C4.npz", 4096, 32)])
+def test_full_iteration_vs_oracle(torch_cuda, oracle_core, name, K, seed):
+    """Every candidate of a full C3 / C4 MPPI iteration (the headline batch, K+1
+    rows, H=50, ring) against the FP64 oracle on the same noise: discrete decisions
+    exact on every rollout away from a near-tie, states/costs within RTOL, and the
+    u* of the device update against the oracle's (softmax over FP32-vs-FP64 costs
+    at lambda = 0.05 is near-argmax: stated tolerance 5e-3)."""
+    import torch
+    from oracle import planner
+    from paper_2509_16079_b200.device import mppi_combine
+    sc = golden(name)
+    plan, noise, gpu = _device_iteration(torch, sc, K, seed)
+    ref = _oracle_iteration(oracle_core, sc, noise)
+    near = (ref["gate_margin"] < GATE_DELTA) | (ref["ring_margin"] < RING_DELTA)
+    clean = ~near
+    differ = (gpu["status"] != ref["status"]) | (gpu["shed_mask"].astype(np.uint64) != ref["shed_mask"])
+    ok = clean & (ref["status"] == 0)
+    rel = np.abs(gpu["cost"][ok] - ref["cost"][ok]) / np.maximum(1.0, np.abs(ref["cost"][ok]))
+    print(f"{name} K={K}: {int(near.sum())} near-tie rollouts of {K + 1} "
+          f"({int((differ & near).sum())} decided differently), {int((ref['status'] != 0).sum())} failed, "
+          f"max cost rel err {rel.max():.2e}")
+    np.testing.assert_array_equal(gpu["status"][clean], ref["status"][clean])
+    np.testing.assert_array_equal(gpu["shed_mask"][clean].astype(np.uint64), ref["shed_mask"][clean])
+    np.testing.assert_array_equal(gpu["n_final"][clean], ref["n_final"][clean])
+    assert_close(gpu["finals"][ok], ref["finals"][ok], what="finals")
+    assert_close(gpu["cost"][ok], ref["cost"][ok], what="cost")
+    dev = torch.device("cuda")
+    us = torch.as_tensor(np.ascontiguousarray(sc["warm"]), device=dev)
+    part = plan.mppi_partial(torch.as_tensor(gpu["cost"], device=dev), us,
+                             torch.as_tensor(noise[0], device=dev), 2.0, 0.05)
+    new = torch.empty_like(us)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    mppi_combine(part.view(1, -1), 0.05, new, flag)
+    torch.cuda.synchronize()
+    assert flag.item() == 0
+    u_ref = planner.weighted_mean(ref["cand"], ref["cost"], 0.05)
+    u_gpu = new.cpu().numpy()
+    print(f"  u* max rel err vs oracle {np.max(np.abs(u_gpu - u_ref) / np.maximum(1.0, np.abs(u_ref))):.2e}")
+    assert_close(u_gpu, u_ref, rtol=5e-3, what="u*")
+
+
 def test_mppi_update_vs_oracle(torch_cuda, oracle_core):
     """Softmax weights and u* from the device partial + combine kernels."""
     import torch
