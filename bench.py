@@ -269,6 +269,11 @@ def extras(torch, dev, sc, flat, plan, mp):
     for i in range(3):
         rp.replan(req, cfg_r, eng_r, np.random.default_rng(1 + i))
     out["replan_cycle_ms_e2e"] = 1e3 * (time.perf_counter() - t0) / 3
+    rp.replan(req, cfg_r, eng_r, mppi_mod.DeviceNoise(0))
+    t0 = time.perf_counter()
+    for i in range(3):
+        rp.replan(req, cfg_r, eng_r, mppi_mod.DeviceNoise(1 + i))
+    out["replan_cycle_ms_e2e_device_noise"] = 1e3 * (time.perf_counter() - t0) / 3
     # C5: Biot-Savart stress sweep, K=16384 rollouts, attached flow (no shedding, fixed N)
     sweep = {}
     rng = np.random.default_rng(11)

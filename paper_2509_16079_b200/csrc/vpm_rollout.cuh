@@ -1214,8 +1214,8 @@ __global__ void mppi_combine_kernel(const double *__restrict__ parts, int W, int
 // ---- device noise (performance mode) ----------------------------------
 // Standard normals for rows [row_begin, row_begin + rows) of one iteration's (K, T)
 // MPPI noise matrix.  One thread per (row, pair of steps): counter-based
-// Philox4x32-10 keyed by seed, subsequence = global noise row, offset = the
-// iteration's block of 4 ceil(T/2) draws + 4 per pair, Box-Muller in FP64
+// Philox4x32-10 keyed by seed, subsequence = global noise row, offset = iteration
+// x 2^32 + 4 per pair (iterations never overlap, whatever T), Box-Muller in FP64
 // (curand_normal2_double).  The value at (g, t) depends only on (seed, iteration,
 // g, t), so every sharding of the rows draws the same numbers; writes coalesce.
 __global__ void noise_philox_kernel(unsigned long long seed, unsigned long long iteration,
@@ -1225,8 +1225,8 @@ __global__ void noise_philox_kernel(unsigned long long seed, unsigned long long 
   if (idx >= (long long)rows * P) return;
   const int r = (int)(idx / P), pr = (int)(idx - (long long)r * P);
   curandStatePhilox4_32_10_t st;
-  curand_init(seed, (unsigned long long)(row_begin + r),
-              iteration * 4ull * (unsigned long long)P + 4ull * (unsigned long long)pr, &st);
+  curand_init(seed, (unsigned long long)(row_begin + r), (iteration << 32) + 4ull * (unsigned long long)pr,
+              &st);
   const double2 v = curand_normal2_double(&st);
   double *o = out + (size_t)r * T + 2 * pr;
   o[0] = v.x;

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import mppi
 from .config import ExperimentConfig
-from .device import policy_fit
+from .device import noise_philox, policy_fit
 from .policy import NominalTrajectory, Policy, RankDeficientData, build_policy
 from .rollout import Engine
 from .vpm import FluidState
@@ -83,6 +83,9 @@ def replan(req: ReplanRequest, cfg: ExperimentConfig, engine: Engine,
     cycle turns out to have failed at such a point, the generator is rewound and
     exactly the draws the reference made before failing are replayed, so the
     caller's generator ends in the reference's state either way.
+    With ``rng = mppi.DeviceNoise(seed)`` (performance mode) every draw -- the MPPI
+    noise and the cloud's dx0 / du -- is made on the device instead and no host
+    random numbers are generated.
     """
     torch, plan, dev, f64 = _dev(engine)
     with plan.lock:
@@ -132,27 +135,42 @@ def _replan_locked(torch, plan, dev, f64, req, cfg, engine, rng):
     # 2./3. the success path's draws and the MPPI iterations (mppi.py:62-84),
     # pipelined: each iteration's noise is drawn on the host and copied while the
     # device runs the previous launch; one failure flag per iteration
-    saved = rng.bit_generator.state
+    # performance mode (mppi.DeviceNoise): every draw on the device, no host RNG
+    devnoise = isinstance(rng, mppi.DeviceNoise)
+    saved = None if devnoise else rng.bit_generator.state
     flags = torch.zeros(max(iters, 1), dtype=torch.int32, device=dev)
     if run_mppi:
         scratch = {"cost": torch.empty(K + 1, dtype=torch.float64, device=dev),
                    "partial": torch.empty(H + 2, dtype=torch.float64, device=dev)}
+        d_buf = torch.empty((K, H), dtype=torch.float64, device=dev) if devnoise else None
         for i in range(iters):
-            lo = nh + i * n_it
-            hv[lo:lo + n_it] = rng.normal(0.0, 1.0, (K, H)).ravel()
-            d_noise = host[lo:lo + n_it].to(dev, non_blocking=True).view(K, H)
+            if devnoise:
+                d_noise = noise_philox(rng.seed, rng.iteration + i, d_buf)
+            else:
+                lo = nh + i * n_it
+                hv[lo:lo + n_it] = rng.normal(0.0, 1.0, (K, H)).ravel()
+                d_noise = host[lo:lo + n_it].to(dev, non_blocking=True).view(K, H)
             scratch["flag"] = flags[i:i + 1]
             plan.mppi_iteration(x0, u, d_noise, mc.input_stdev, K + 1, mc.temperature, q, xp, scratch)
-    lo = nh + iters * n_it
-    dx0 = rng.normal(0.0, 1.0, (k, 7))
-    du = rng.normal(0.0, 1.0, (k, H))
-    cx = hv[lo:lo + (k + 1) * 7].reshape(k + 1, 7)
-    cu = hv[lo + (k + 1) * 7:lo + n_cloud].reshape(k + 1, H)
-    cx[0], cx[1:] = 0.0, dx0  # row 0: the nominal, unperturbed
-    cu[0], cu[1:] = 0.0, du
-    dcl = host[lo:lo + n_cloud].to(dev, non_blocking=True)
-    d_cx = dcl[:(k + 1) * 7].view(k + 1, 7)
-    d_cu = dcl[(k + 1) * 7:].view(k + 1, H)
+    if devnoise:
+        dcl = torch.zeros(n_cloud, dtype=torch.float64, device=dev)  # row 0: the nominal
+        d_cx = dcl[:(k + 1) * 7].view(k + 1, 7)
+        d_cu = dcl[(k + 1) * 7:].view(k + 1, H)
+        if k > 0:
+            noise_philox(rng.seed, rng.iteration + iters, d_cx[1:])
+            noise_philox(rng.seed, rng.iteration + iters + 1, d_cu[1:])
+        rng.iteration += iters + 2
+    else:
+        lo = nh + iters * n_it
+        dx0 = rng.normal(0.0, 1.0, (k, 7))
+        du = rng.normal(0.0, 1.0, (k, H))
+        cx = hv[lo:lo + (k + 1) * 7].reshape(k + 1, 7)
+        cu = hv[lo + (k + 1) * 7:lo + n_cloud].reshape(k + 1, H)
+        cx[0], cx[1:] = 0.0, dx0  # row 0: the nominal, unperturbed
+        cu[0], cu[1:] = 0.0, du
+        dcl = host[lo:lo + n_cloud].to(dev, non_blocking=True)
+        d_cx = dcl[:(k + 1) * 7].view(k + 1, 7)
+        d_cu = dcl[(k + 1) * 7:].view(k + 1, H)
     # 4. nominal (row 0) + perturbed cloud (rows 1..k) in one launch (policy.py:66-91)
     cstat, ctraj = plan.cloud(x0, d_cx, d_sx, u, d_cu, sc.input_stdev)
     traj = ctraj[0]
@@ -162,6 +180,14 @@ def _replan_locked(torch, plan, dev, f64, req, cfg, engine, rng):
                                            d_qf)
     # 6. the one synchronisation: every decision the reference makes, in its order
     ints = torch.cat([pstat.view(1), flags.to(torch.int64), cstat, fflag[:1].to(torch.int64)]).cpu().numpy()
+    if devnoise:  # no generator to leave in the reference's state
+        st = ints[1 + max(iters, 1):1 + max(iters, 1) + k + 1]
+        if ints[0] != 0 or (run_mppi and np.any(ints[1:1 + iters] != 0)) or st[0] != 0:
+            return None
+        if int((st[1:] == 0).sum()) < 6 or ints[-1] != 0:
+            return None
+        nominal = NominalTrajectory(states=traj.cpu().numpy(), inputs=u.cpu().numpy(), dt=dt, t_start=t_new)
+        return Policy(gains=d_gain.cpu().numpy(), nominal=nominal, q_final=np.asarray(sc.q_final, dtype=float))
     if ints[0] != 0:
         rng.bit_generator.state = saved  # projection failed before any draw
         return None

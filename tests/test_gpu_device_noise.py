@@ -83,3 +83,30 @@ def test_optimize_with_device_noise_equals_host_pipeline(torch_cuda):
     u2 = mppi.optimize(x0, fl, warm, cfg.mppi, eng, mppi.DeviceNoise(5, iteration=3), iterations=2)
     u3 = mppi.optimize(x0, fl, warm, cfg.mppi, eng, dn, iterations=2)
     np.testing.assert_array_equal(u2, u3)
+
+
+def test_replan_with_device_noise(torch_cuda):
+    """nmpc.replan in performance mode: a policy comes back, the same seed gives the
+    same policy, and the noise counter advances by iterations + 2 (cloud dx0, du)."""
+    import os
+
+    from conftest import GOLDEN
+    from paper_2509_16079_b200 import config, mppi, replan as rp, rollout, vpm
+    from paper_2509_16079_b200.policy import NominalTrajectory, Policy
+    with np.load(os.path.join(GOLDEN, "nmpc_replan.npz")) as z:
+        gr = {k: z[k] for k in z.files}
+    cfg = config.ExperimentConfig()
+    eng = rollout.Engine.from_config(cfg)
+    pol = Policy(gains=gr["boot_gains"], nominal=NominalTrajectory(gr["boot_states"], gr["boot_inputs"], 0.01))
+    req = rp.ReplanRequest(x=np.asarray(cfg.scenario.x0, float), fluid=vpm.FluidState.empty(cfg.vpm),
+                           policy=pol, t=0.0, t_proj=10)
+    dn = mppi.DeviceNoise(9)
+    a = rp.replan(req, cfg, eng, dn)
+    assert dn.iteration == cfg.mppi.iterations + 2
+    b = rp.replan(req, cfg, eng, mppi.DeviceNoise(9))
+    assert a is not None and b is not None
+    np.testing.assert_array_equal(a.gains, b.gains)
+    np.testing.assert_array_equal(a.nominal.inputs, b.nominal.inputs)
+    assert np.isfinite(a.gains).all() and np.abs(a.nominal.inputs).max() <= cfg.glider.u_limit
+    c = rp.replan(req, cfg, eng, dn)  # next counter block: a different plan
+    assert c is None or not np.array_equal(c.nominal.inputs, a.nominal.inputs)
