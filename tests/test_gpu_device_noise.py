@@ -110,3 +110,18 @@ def test_replan_with_device_noise(torch_cuda):
     assert np.isfinite(a.gains).all() and np.abs(a.nominal.inputs).max() <= cfg.glider.u_limit
     c = rp.replan(req, cfg, eng, dn)  # next counter block: a different plan
     assert c is None or not np.array_equal(c.nominal.inputs, a.nominal.inputs)
+
+
+def test_bootstrap_with_device_noise(torch_cuda):
+    """bootstrap_policy (annealed MPPI + nominal + build_policy) runs end to end with
+    a DeviceNoise generator and is deterministic."""
+    from paper_2509_16079_b200 import config, mppi, replan as rp, rollout
+    cfg = config.ExperimentConfig()
+    cfg.mppi.batch = 128
+    cfg.scenario.bootstrap_iterations = 3
+    eng = rollout.Engine.from_config(cfg)
+    a = rp.bootstrap_policy(cfg, eng, mppi.DeviceNoise(2))
+    b = rp.bootstrap_policy(cfg, eng, mppi.DeviceNoise(2))
+    np.testing.assert_array_equal(a.gains, b.gains)
+    np.testing.assert_array_equal(a.nominal.inputs, b.nominal.inputs)
+    assert np.isfinite(a.gains).all()
