@@ -87,12 +87,12 @@ def replan(req: ReplanRequest, cfg: ExperimentConfig, engine: Engine,
     noise and the cloud's dx0 / du -- is made on the device instead and no host
     random numbers are generated.
     """
-    torch, plan, dev, f64 = _dev(engine)
+    torch, plan, dev, _ = _dev(engine)
     with plan.lock:
-        return _replan_locked(torch, plan, dev, f64, req, cfg, engine, rng)
+        return _replan_locked(torch, plan, dev, req, cfg, engine, rng)
 
 
-def _replan_locked(torch, plan, dev, f64, req, cfg, engine, rng):
+def _replan_locked(torch, plan, dev, req, cfg, engine, rng):
     dt = engine.cfg.dt
     lim = engine.params.u_limit
     old = req.policy.nominal
