@@ -73,78 +73,59 @@ def optimize(x0, fluid: FluidState, warm_start, cfg: MppiConfig, engine: Engine,
     import torch
     plan = engine_plan(engine)
     with plan.lock:
-        if isinstance(rng, DeviceNoise):
-            return _optimize_device_noise(torch, plan, x0, fluid, u, cfg, rng, iters, H, K)
         return _optimize_locked(torch, plan, x0, fluid, u, cfg, rng, iters, H, K)
 
 
 class DeviceNoise:
-    """Performance mode for :func:`optimize`: pass ``DeviceNoise(seed)`` as ``rng``
-    and the control-perturbation noise is drawn on the device (counter-based
-    Philox keyed by (seed, iteration, row), ``vpm_noise_philox``) instead of by
-    numpy on the host -- no host RNG time and no host-to-device noise copy.  The
-    numbers differ from numpy's, so reference parity uses a numpy Generator.
-    ``iteration`` advances by one per MPPI iteration drawn, across calls."""
+    """Performance mode for :func:`optimize` (and ``replan`` / ``build_policy``):
+    pass ``DeviceNoise(seed)`` as ``rng`` and the control-perturbation noise is
+    drawn on the device (counter-based Philox keyed by (seed, iteration, row),
+    ``vpm_noise_philox``) instead of by numpy on the host -- no host RNG time and no
+    host-to-device noise copy.  The numbers differ from numpy's, so reference parity
+    uses a numpy Generator.  ``iteration`` advances by one per block drawn, across
+    calls."""
 
     def __init__(self, seed: int, iteration: int = 0):
         self.seed = int(seed)
         self.iteration = int(iteration)
 
 
-def _optimize_device_noise(torch, plan, x0, fluid, u, cfg, rng, iters, H, K):
-    from .device import noise_philox
-    dev = torch.device("cuda", plan.device)
-    plan.set_fluid(fluid)
-    host = plan.staging(H + 21)
-    hv = host.numpy()
-    hv[:H] = u
-    hv[H:H + 7] = np.asarray(x0, dtype=float)
-    hv[H + 7:H + 14] = np.asarray(cfg.q_terminal, dtype=float)
-    hv[H + 14:H + 21] = np.asarray(cfg.x_perch, dtype=float)
-    head = host[:H + 21].to(dev, non_blocking=True)
-    u_dev, x0d, q, xp = head[:H].clone(), head[H:H + 7], head[H + 7:H + 14], head[H + 14:H + 21]
-    flags = torch.zeros(iters, dtype=torch.int32, device=dev)
-    noise = torch.empty((K, H), dtype=torch.float64, device=dev)
-    scratch = {"cost": torch.empty(K + 1, dtype=torch.float64, device=dev),
-               "partial": torch.empty(H + 2, dtype=torch.float64, device=dev)}
-    for i in range(iters):
-        noise_philox(rng.seed, rng.iteration + i, noise)
-        scratch["flag"] = flags[i:i + 1]
-        plan.mppi_iteration(x0d, u_dev, noise, cfg.input_stdev, K + 1, cfg.temperature, q, xp, scratch)
-    rng.iteration += iters
-    out = torch.cat([u_dev, flags.to(torch.float64)]).cpu().numpy()
-    if np.any(out[H:] != 0):
-        raise ValueError("all sampled rollouts failed (infinite cost)")
-    return out[:H].copy()
-
-
 def _optimize_locked(torch, plan, x0, fluid, u, cfg, rng, iters, H, K):
+    from .device import noise_philox
+    devnoise = isinstance(rng, DeviceNoise)
     dev = torch.device("cuda", plan.device)
     plan.set_fluid(fluid)
-    n_it = K * H
-    host = plan.staging(H + 7 + 14 + iters * n_it)
+    n_it = 0 if devnoise else K * H
+    host = plan.staging(H + 21 + iters * n_it)
     hv = host.numpy()
     hv[:H] = u
     hv[H:H + 7] = np.asarray(x0, dtype=float)
     hv[H + 7:H + 14] = np.asarray(cfg.q_terminal, dtype=float)
     hv[H + 14:H + 21] = np.asarray(cfg.x_perch, dtype=float)
-    head = host[:H + 21].to(dev, non_blocking=True)
+    head = host[:H + 21].to(dev, non_blocking=True)  # one pinned, non-blocking upload
     u_dev, x0d, q, xp = head[:H].clone(), head[H:H + 7], head[H + 7:H + 14], head[H + 14:H + 21]
     flags = torch.zeros(iters, dtype=torch.int32, device=dev)
     scratch = {"cost": torch.empty(K + 1, dtype=torch.float64, device=dev),
                "partial": torch.empty(H + 2, dtype=torch.float64, device=dev)}
-    saved = rng.bit_generator.state
+    d_buf = torch.empty((K, H), dtype=torch.float64, device=dev) if devnoise else None
+    saved = None if devnoise else rng.bit_generator.state
     for i in range(iters):
-        lo = H + 21 + i * n_it
-        hv[lo:lo + n_it] = rng.normal(0.0, 1.0, (K, H)).ravel()
-        d_noise = host[lo:lo + n_it].to(dev, non_blocking=True).view(K, H)
+        if devnoise:
+            d_noise = noise_philox(rng.seed, rng.iteration + i, d_buf)
+        else:
+            lo = H + 21 + i * n_it
+            hv[lo:lo + n_it] = rng.normal(0.0, 1.0, (K, H)).ravel()
+            d_noise = host[lo:lo + n_it].to(dev, non_blocking=True).view(K, H)
         scratch["flag"] = flags[i:i + 1]
         plan.mppi_iteration(x0d, u_dev, d_noise, cfg.input_stdev, K + 1, cfg.temperature, q, xp, scratch)
+    if devnoise:
+        rng.iteration += iters
     out = torch.cat([u_dev, flags.to(torch.float64)]).cpu().numpy()
     bad = np.nonzero(out[H:] != 0)[0]
     if bad.size:
-        rng.bit_generator.state = saved
-        rng.normal(0.0, 1.0, (int(bad[0]) + 1, K, H))
+        if not devnoise:  # leave the generator where the reference's raise leaves it
+            rng.bit_generator.state = saved
+            rng.normal(0.0, 1.0, (int(bad[0]) + 1, K, H))
         raise ValueError("all sampled rollouts failed (infinite cost)")
     return out[:H].copy()
 
