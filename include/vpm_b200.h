@@ -126,6 +126,11 @@ typedef struct vpm_batch_out {
   uint64_t *shed_mask;  /* (rows) bit t set when step t shed */
   int32_t *n_final;     /* (rows) final wake size */
   int64_t *interactions;/* (rows) regularised Biot-Savart interactions evaluated */
+  uint64_t *shed_mask_hi; /* (rows) bit t-64 set when step t (64 <= t < 128) shed */
+  uint64_t *wake_hash;  /* (rows) wake-index signature: per-step (wake size, ring-core
+                           indices, shed flag) chain + final (index, age) sum; parity
+                           diagnostic of the shed / merge / ordered-removal bookkeeping
+                           (_core.pyx:157-172, 322-373) */
 } vpm_batch_out;
 
 /* Device batch of rows [row_begin, row_end) of a B_total-row candidate set.

@@ -12,5 +12,4 @@ Nothing in ``paper_2509_16079_b200`` imports this package.  Only ``tests/``,
   ``policy.py:66-266`` driven by :mod:`oracle.core`.
 * :mod:`oracle.refcore` -- loader for ``oracle/_ref/_core*.so``, the reference's
   own Cython core compiled by ``oracle/build_ref.sh``.
-* :mod:`oracle.scenario` -- synthetic perching scenarios.
 """

@@ -26,3 +26,14 @@ cython -3 "$SRC" -o "$OUT/_core.c"
   -DNPY_NO_DEPRECATED_API=NPY_1_7_API_VERSION \
   "$OUT/_core.c" -o "$OUT/_core$EXT_SUFFIX" -lgomp
 echo "built $OUT/_core$EXT_SUFFIX"
+# Stage the unmodified reference package (pure Python + numpy) under oracle/_ref/pkg
+# so the drop-in test (tests/test_gpu_dropin.py) can run the reference's own
+# mppi.optimize / policy.build_policy / Engine / nmpc.control_loop on the GPU box
+# with the CUDA stepping module installed as its _accel._core.  Git-ignored (never
+# in history); travels with the gpurun snapshot like the compiled core.
+rm -rf "$OUT/pkg"
+mkdir -p "$OUT/pkg"
+cp -r "${REF_ROOT:-/root/reference}/pkg/src/perchsim" "$OUT/pkg/perchsim"
+find "$OUT/pkg" -name __pycache__ -prune -exec rm -rf {} +
+chmod -R u+w "$OUT/pkg"
+echo "staged $OUT/pkg/perchsim"

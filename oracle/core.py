@@ -56,7 +56,7 @@ def lib():
         L.oracle_batch_rollout.argtypes = [
             _D, C.c_int, _D, C.c_int, C.c_int, _D, _D, _I64, C.c_int, C.c_int, C.c_int,
             _D, _D, C.c_int, C.c_double, _D, _I64, _D, _I64, _D, _D, _U64, _I32, _D, _D,
-            _I64, C.c_int]
+            _I64, _U64, _U64, C.c_int]
         L.oracle_rollout.restype = C.c_int64
         L.oracle_rollout.argtypes = [
             _D, _D, C.c_int, _D, _D, _I64, C.c_int, C.c_int, C.c_int, _D, _D, C.c_int,
@@ -151,12 +151,14 @@ def batch_rollout_diag(x0, controls, wake_pos, wake_gamma, wake_age, n_wake, rin
                trajs=np.zeros((B, T + 1, 7)) if record else None,
                shed_mask=np.zeros(B, dtype=np.uint64), n_final=np.zeros(B, dtype=np.int32),
                gate_margin=np.zeros(B), ring_margin=np.zeros(B),
-               n_steps=np.zeros((B, T), dtype=np.int64) if per_step_n else None)
+               n_steps=np.zeros((B, T), dtype=np.int64) if per_step_n else None,
+               shed_mask_hi=np.zeros(B, dtype=np.uint64), wake_hash=np.zeros(B, dtype=np.uint64))
     lib().oracle_batch_rollout(
         _p(x0a, _D), stride, _p(ctrl, _D), B, T, *fa, _p(ip, _I64), _p(fp, _D),
         _p(out["status"], _I64), _p(out["finals"], _D), _p(out["trajs"], _D),
         _p(out["shed_mask"], _U64), _p(out["n_final"], _I32), _p(out["gate_margin"], _D),
-        _p(out["ring_margin"], _D), _p(out["n_steps"], _I64), int(workers))
+        _p(out["ring_margin"], _D), _p(out["n_steps"], _I64), _p(out["shed_mask_hi"], _U64),
+        _p(out["wake_hash"], _U64), int(workers))
     return out
 
 

@@ -60,9 +60,30 @@ typedef struct {
 typedef struct {
   double gate_margin; /* min | |aoa| - crit |, | |aoa| - pi/2 | over steps */
   double ring_margin; /* min distance of the intersection parameters from 0/1 */
-  uint64_t shed_mask; /* bit t set when step t shed */
+  uint64_t shed_mask; /* bit t set when step t shed (t < 64) */
+  uint64_t shed_hi;   /* bit t-64 set when step t shed (64 <= t < 128) */
+  uint64_t whash;     /* wake-index signature chain (sig_step) */
   int step;           /* step index inside the rollout */
 } Diag;
+
+/* Wake-index signature, the same function the CUDA kernel evaluates
+ * (paper_2509_16079_b200/csrc/vpm_rollout.cuh wake_sig_*): after each step's shed,
+ * merge and ring termination (_core.pyx:322-373) the chain absorbs (wake size,
+ * ring-core indices, shed flag); at the end the sum over the final wake of
+ * mix(index, age) is folded in.  Equal signatures = same shed steps, same merges
+ * per step, same final index -> age order (the ordered-removal contract of
+ * remove_particle, _core.pyx:157-172). */
+static uint64_t sig_mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static uint64_t sig_step(uint64_t h, int n, int ra, int rb, int shed) {
+  uint64_t key = (uint64_t)(uint32_t)n | ((uint64_t)(shed != 0) << 31) |
+                 ((uint64_t)(uint16_t)(ra + 1) << 32) | ((uint64_t)(uint16_t)(rb + 1) << 48);
+  return sig_mix(h ^ key);
+}
 
 static void cfg_load(Cfg *c, const int64_t *ip, const double *fp) {
   c->nb = (int)ip[0];
@@ -256,6 +277,7 @@ static int coupled_step(double *xs, double u, Wake *w, const Cfg *c, int integra
     w->x[k + 1] = tx; w->z[k + 1] = tz; w->g[k + 1] = gam[nb + 1]; w->age[k + 1] = 0.0;
     w->n = k + 2;
     if (dg && dg->step < 64) dg->shed_mask |= (uint64_t)1 << dg->step;
+    if (dg && dg->step >= 64 && dg->step < 128) dg->shed_hi |= (uint64_t)1 << (dg->step - 64);
   }
 
   /* merge the two oldest non-ring particles until at cap, _core.pyx:336-357,
@@ -294,6 +316,7 @@ static int coupled_step(double *xs, double u, Wake *w, const Cfg *c, int integra
       w->ring_b = -1;
     }
   }
+  if (dg) dg->whash = sig_step(dg->whash, w->n, w->ring_a, w->ring_b, shed);
 
   /* unsteady-Bernoulli panel loads about the wing point, _core.pyx:375-410,
    * vpm.py:580-628 */
@@ -455,7 +478,8 @@ int oracle_batch_rollout(const double *x0, int x0_stride, const double *controls
                          const double *prev_gamma, int n_prev, double prev_lev, const double *ema,
                          const int64_t *iparams, const double *fparams, int64_t *status,
                          double *finals, double *trajs, uint64_t *shed_mask, int32_t *n_final,
-                         double *gate_margin, double *ring_margin, int64_t *nw_steps, int threads) {
+                         double *gate_margin, double *ring_margin, int64_t *nw_steps,
+                         uint64_t *shed_mask_hi, uint64_t *wake_hash, int threads) {
   Cfg c;
   cfg_load(&c, iparams, fparams);
   if (c.nb > OR_MAXNB) return -1;
@@ -471,13 +495,19 @@ int oracle_batch_rollout(const double *x0, int x0_stride, const double *controls
     wake_fork(&w, &s, &c, buf);
     double xs[7];
     memcpy(xs, x0 + (size_t)b * x0_stride, 7 * sizeof(double));
-    Diag dg = {1e300, 1e300, 0, 0};
+    Diag dg = {1e300, 1e300, 0, 0, 0, 0};
     int64_t rc = run_one(xs, controls + (size_t)b * T, T, &w, &c,
                          trajs ? trajs + (size_t)b * (T + 1) * 7 : NULL, buf + 4 * capbuf, &dg,
                          nw_steps ? nw_steps + (size_t)b * T : NULL);
     if (status) status[b] = rc;
     if (finals) memcpy(finals + 7 * (size_t)b, xs, 7 * sizeof(double));
     if (shed_mask) shed_mask[b] = dg.shed_mask;
+    if (shed_mask_hi) shed_mask_hi[b] = dg.shed_hi;
+    if (wake_hash) {
+      uint64_t hs = 0;
+      for (int i = 0; i < w.n; ++i) hs += sig_mix(((uint64_t)(uint32_t)i << 32) | (uint64_t)(uint32_t)(int64_t)w.age[i]);
+      wake_hash[b] = sig_mix(dg.whash ^ hs);
+    }
     if (n_final) n_final[b] = w.n;
     if (gate_margin) gate_margin[b] = dg.gate_margin;
     if (ring_margin) ring_margin[b] = dg.ring_margin;

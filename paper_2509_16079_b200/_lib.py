@@ -72,7 +72,7 @@ class VpmFluidOut(C.Structure):
 class VpmBatchOut(C.Structure):
     _fields_ = [("status", C.c_void_p), ("finals", C.c_void_p), ("trajs", C.c_void_p),
                 ("cost", C.c_void_p), ("shed_mask", C.c_void_p), ("n_final", C.c_void_p),
-                ("interactions", C.c_void_p)]
+                ("interactions", C.c_void_p), ("shed_mask_hi", C.c_void_p), ("wake_hash", C.c_void_p)]
 
 
 _lib = None

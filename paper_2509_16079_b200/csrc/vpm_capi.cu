@@ -508,6 +508,8 @@ int vpm_plan_batch(vpm_plan *p, const double *d_x0, int x0_stride, const double 
     a.trajs = o->trajs;
     a.cost = (d_q && d_xperch) ? o->cost : nullptr;
     a.shed_mask = o->shed_mask;
+    a.shed_mask_hi = o->shed_mask_hi;
+    a.wake_hash = o->wake_hash;
     a.n_final = o->n_final;
     a.inter = o->interactions;
   }

@@ -161,7 +161,9 @@ struct Args {
   int64_t *status;
   double *finals, *trajs, *cost;
   const double *q, *xp;
-  uint64_t *shed_mask;
+  uint64_t *shed_mask;     // steps 0..63
+  uint64_t *shed_mask_hi;  // steps 64..127
+  uint64_t *wake_hash;     // wake-index signature (wake_sig_* below)
   int32_t *n_final;
   int64_t *inter;
   int32_t *rc_out;
@@ -194,7 +196,8 @@ struct Ctl {
   double el[4];
   double th_sn, th_cs;
   long long inter;
-  unsigned long long shed_mask;
+  unsigned long long shed_mask, shed_hi;
+  unsigned long long whash, hsum;  // wake-index signature: step chain, final age sum
 };
 
 // ---- shared-memory layout (host computes the same size) ----------------------
@@ -239,6 +242,28 @@ __device__ __forceinline__ float rsqrt_mufu(float v) {
   float r;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
   return r;
+}
+
+// Wake-index signature (parity diagnostic, oracle/vpm_oracle.c computes the same):
+// a chain over the steps of (wake size, ring-core indices, shed flag) after each
+// step's shed / merge / ring termination (_core.pyx:322-373), then the sum over the
+// final wake of mix(index, age) -- equal signatures mean the same shed steps, the
+// same merge count per step and the same final (index -> age) order.
+__host__ __device__ __forceinline__ unsigned long long wake_sig_mix(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ unsigned long long wake_sig_step(unsigned long long h, int n, int ra,
+                                                                     int rb, int shed) {
+  const unsigned long long key = (unsigned long long)(unsigned)n | ((unsigned long long)(shed != 0) << 31) |
+                                 ((unsigned long long)(unsigned short)(ra + 1) << 32) |
+                                 ((unsigned long long)(unsigned short)(rb + 1) << 48);
+  return wake_sig_mix(h ^ key);
+}
+__host__ __device__ __forceinline__ unsigned long long wake_sig_elem(int c, int age) {
+  return wake_sig_mix(((unsigned long long)(unsigned)c << 32) | (unsigned long long)(unsigned)age);
 }
 
 // One regularised Biot-Savart interaction (_core.pyx:89-97) in the form every
@@ -498,6 +523,9 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
       ctl->rc = 0;
       ctl->inter = 0;
       ctl->shed_mask = 0ull;
+      ctl->shed_hi = 0ull;
+      ctl->whash = 0ull;
+      ctl->hsum = 0ull;
       ctl->fwx = ctl->fwz = ctl->mw = 0.0;
       ctl->hp = 0;
       ctl->shed = ctl->rev = 0;
@@ -987,6 +1015,8 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           ctl->mcnt = min(MC, max(0, n_live_next + 3 - P.cap));
           ctl->cur = cur ^ 1;
           if (shed && t < 64) ctl->shed_mask |= 1ull << t;
+          if (shed && t >= 64 && t < 128) ctl->shed_hi |= 1ull << (t - 64);
+          ctl->whash = wake_sig_step(ctl->whash, n_live_next, ra2, rb2, shed);
           ctl->inter += (long long)nl * (nl - 1) + (long long)n_prev * nl + (long long)nb * nl +
                         (long long)nb * n_live_next;
         }
@@ -1001,10 +1031,23 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
   PHASE_FLUSH;
 
   // ---- epilogue: outputs
+  if (a.wake_hash) {
+    // final (index, age) sum of the signature; integer sums are order-free
+    const int nl = ctl->n_live, nh = ctl->n_holes;
+    const float4 *wfin = wbuf + ctl->cur * L.capbuf;
+    unsigned long long hs = 0ull;
+    for (int c = tid; c < nl; c += NT) hs += wake_sig_elem(c, __float_as_int(wfin[raw_index(c, ctl->holes, nh)].w));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
+    if (lane == 0) atomicAdd(&ctl->hsum, hs);
+    __syncthreads();
+  }
   if (tid == 0) {
     if (a.status) a.status[row] = ctl->status;
     if (a.rc_out) a.rc_out[row] = ctl->rc;
     if (a.shed_mask) a.shed_mask[row] = ctl->shed_mask;
+    if (a.shed_mask_hi) a.shed_mask_hi[row] = ctl->shed_hi;
+    if (a.wake_hash) a.wake_hash[row] = wake_sig_mix(ctl->whash ^ ctl->hsum);
     if (a.n_final) a.n_final[row] = ctl->n_live;
     if (a.inter) a.inter[row] = ctl->inter;
     if (a.fw_out) { a.fw_out[3 * row] = ctl->fwx; a.fw_out[3 * row + 1] = ctl->fwz; a.fw_out[3 * row + 2] = ctl->mw; }

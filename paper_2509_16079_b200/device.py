@@ -109,9 +109,11 @@ class DevicePlan:
                 o["shed_mask"] = torch.zeros(rows, dtype=torch.int64, device=dev)
                 o["n_final"] = torch.zeros(rows, dtype=torch.int32, device=dev)
                 o["interactions"] = torch.zeros(rows, dtype=torch.int64, device=dev)
+                o["shed_mask_hi"] = torch.zeros(rows, dtype=torch.int64, device=dev)
+                o["wake_hash"] = torch.zeros(rows, dtype=torch.int64, device=dev)
         bo = VpmBatchOut(_p(o.get("status")), _p(o.get("finals")), _p(o.get("trajs")),
                          _p(o.get("cost")), _p(o.get("shed_mask")), _p(o.get("n_final")),
-                         _p(o.get("interactions")))
+                         _p(o.get("interactions")), _p(o.get("shed_mask_hi")), _p(o.get("wake_hash")))
         stride = 7 if x0.dim() == 2 else 0
         check(_lib.lib().vpm_plan_batch(
             self.handle, _p(x0), stride, _p(controls), _p(ustar), _p(noise), float(sigma),

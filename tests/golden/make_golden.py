@@ -18,7 +18,12 @@ Fixtures
   mppi_C2.npz      mppi.optimize, 3 iterations, C2 scenario, rng seed 0
   mppi_C3s.npz     one MPPI iteration with K=48 on the C3 scenario, rng seed 1
   policy_C2.npz    policy.build_policy around the C2 nominal, rng seed 2
+  wake_sig.npz     (``make_golden.py wake_sig``) per-step shed / merge / ring
+                   bookkeeping and final wake ages of MPPI candidate rollouts on the
+                   C3 and C4 ring scenarios (H=50) and a C3 H=100 set, stepped with
+                   the reference's Engine.step + the run_rollout envelope test
 """
+
 from __future__ import annotations
 
 import os
@@ -174,7 +179,61 @@ def make_replan():
          new_states=new.nominal.states, new_inputs=new.nominal.inputs, new_t_start=new.t_start)
 
 
+def make_wake_sig():
+    """Reference-side pin of the wake-index signature (tests/wake_sig.py): every
+    rollout is stepped with the reference's Engine.step (numpy backend) and the
+    run_rollout envelope / failure test (_core.pyx:465-491, reference.py:85-111);
+    after each completed step the wake size, ring-core indices and the shed flag
+    (a particle of age 0 exists: shed particles enter at age 0 after the step's
+    ageing, _core.pyx:222-226, 322-334) are recorded, plus the final wake ages."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    from wake_sig import signature
+    out = {}
+    for tag, name, K, H_, seed in (("c3", "scenario_C3.npz", 8, 50, 51), ("c4", "scenario_C4.npz", 8, 50, 52),
+                                   ("c3long", "scenario_C3.npz", 4, 100, 53)):
+        with np.load(os.path.join(HERE, name)) as z:
+            sc = {k: z[k] for k in z.files}
+        cap = int(sc["cap"])
+        cfg, eng = engine(cap)
+        fl0 = vpm.FluidState.empty(cfg.vpm)
+        n0 = int(sc["n_wake"])
+        fl0.wake_pos[:n0], fl0.wake_gamma[:n0], fl0.wake_age[:n0] = (sc["wake_pos"][:n0], sc["wake_gamma"][:n0],
+                                                                     sc["wake_age"][:n0])
+        fl0.n_wake, fl0.ring_a, fl0.ring_b = n0, int(sc["ring_a"]), int(sc["ring_b"])
+        m = int(sc["n_prev"])
+        fl0.prev_pos[:m], fl0.prev_gamma[:m], fl0.n_prev = sc["prev_pos"][:m], sc["prev_gamma"][:m], m
+        fl0.prev_lev_gamma, fl0.unsteady_ema[:] = float(sc["prev_lev"]), sc["ema"]
+        warm = np.full(H_, -6.0)
+        noise = np.random.default_rng(seed).normal(0.0, 1.0, (K, H_))
+        ctrl = np.clip(warm[None, :] + 2.0 * noise, -15.0, 15.0)
+        status, sigs, nsteps, finals = [], [], [], []
+        for k in range(K):
+            fl, x, st, steps = fl0, X0.copy(), 0, []
+            for t in range(H_):
+                ok, x, fl, _ = eng.step(x, ctrl[k, t], fl)
+                n = fl.n_wake
+                steps.append((n, fl.ring_a, fl.ring_b, bool(np.any(fl.wake_age[:n] == 0))))
+                if (not ok or not np.all(np.isfinite(x)) or abs(x[6]) > 300.0
+                        or np.max(np.abs(x[4:6])) > 80.0):
+                    st = 1 + t
+                    break
+            status.append(st)
+            sigs.append(signature(steps, fl.wake_age[: fl.n_wake]))
+            nsteps.append([s[0] for s in steps] + [-1] * (H_ - len(steps)))
+            finals.append(x)
+            print(tag, k, "status", st, "n", fl.n_wake, "shed steps", sum(s[3] for s in steps))
+        out[tag + "_controls"] = ctrl
+        out[tag + "_status"] = np.array(status, np.int64)
+        out[tag + "_sig"] = np.array(sigs, np.uint64)
+        out[tag + "_n_steps"] = np.array(nsteps, np.int64)
+        out[tag + "_finals"] = np.array(finals)
+    save("wake_sig.npz", **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "wake_sig":
+        make_wake_sig()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "replan":
         make_replan()
         sys.exit(0)

@@ -1,11 +1,32 @@
 """GPU parity: the sm_100a path (through the C ABI) against the reference's golden
-vectors and the FP64 CPU oracle on identical inputs and identical noise.
+vectors, the reference's own compiled core (oracle/_ref) and the FP64 CPU oracle on
+identical inputs and identical noise.
 
-Tolerances (stated, FP32 Biot-Savart vs FP64 reference):
-  * discrete decisions -- status, shed steps (bitmask), final wake size -- exact,
-    except on rollouts whose oracle-recorded gate or ring-termination margin is
-    below GATE_DELTA / RING_DELTA (near-ties, counted and reported, never hidden);
-  * states, costs, u*: |gpu - ref| <= RTOL * max(1, |ref|) with RTOL = 1e-4.
+Tolerances (stated; FP32 Biot-Savart sums and FP32 wake storage vs the
+reference's float64).  Continuous quantities are checked as relative errors:
+
+  * "elementwise":  |gpu - ref| <= rtol |ref| + atol
+  * "normwise":     |gpu - ref| <= rtol max|ref| + atol, the max taken per physical
+    component over the compared set (each state component over all rollouts /
+    steps, u* over the horizon, each wake coordinate over the wake) -- a true
+    relative error of the vector, defined where elementwise ratios are not
+    (components cross zero: a final v_z of -0.045 m/s is reached along a
+    trajectory where v_z spans +-3 m/s).
+
+  quantity                              mode         rtol    atol
+  glider states / finals / trajectories normwise     1e-4    1e-9
+  wake positions / circulations         normwise     1e-4    1e-9
+  wing force / moment                   normwise     1e-4    1e-9
+  terminal costs                        elementwise  1e-4    0
+  planned controls u*                   normwise     1e-4    0
+  normalised MPPI weights               absolute     0       1e-4
+  feedback gains (regression+Riccati)   normwise     1e-4    0
+
+  Discrete decisions -- status, shed steps (128-bit mask), final wake size and the
+  wake-index signature (per-step wake size / ring indices / shed flag + final
+  index -> age order, tests/wake_sig.py) -- are exact, except on rollouts whose
+  oracle-recorded gate or ring-termination margin is below GATE_DELTA /
+  RING_DELTA (near-ties, counted and printed, never hidden).
 """
 import numpy as np
 import pytest
@@ -14,23 +35,40 @@ from conftest import flat_of, golden
 
 pytestmark = pytest.mark.gpu
 
-RTOL = 1e-4
-GATE_DELTA = 1e-4   # rad
-RING_DELTA = 1e-4   # intersection-parameter margin
+GATE_DELTA = 1e-5   # rad, | |aoa| - crit | and | |aoa| - pi/2 |
+RING_DELTA = 1e-5   # intersection-parameter margin
 X0 = np.array([0.0, 0.0, 0.3, 0.0, 7.0, 0.0, 0.0])
+TOL = {  # kind: (mode, rtol, atol)
+    "state": ("norm", 1e-4, 1e-9), "wake_pos": ("norm", 1e-4, 1e-9), "wake_gamma": ("norm", 1e-4, 1e-9),
+    "fw": ("norm", 1e-4, 1e-9), "cost": ("elem", 1e-4, 0.0), "u": ("norm", 1e-4, 0.0),
+    "weight": ("elem", 0.0, 1e-4), "gain": ("norm", 1e-4, 0.0)}
 
 
-def close(a, b, rtol=RTOL):
+def assert_close(a, b, kind="state", what=""):
+    """Relative-error check of TOL[kind]; normwise scales are taken per component
+    (last axis) for arrays of 2+ dimensions, over the whole vector for 1-D ones."""
+    mode, rtol, atol = TOL[kind]
     a, b = np.asarray(a, float), np.asarray(b, float)
-    return np.abs(a - b) <= rtol * np.maximum(1.0, np.abs(b))
-
-
-def assert_close(a, b, rtol=RTOL, what=""):
-    ok = close(a, b, rtol)
+    err = np.abs(a - b)
+    if mode == "norm" and b.size:
+        axes = tuple(range(b.ndim - 1)) if b.ndim >= 2 else None
+        scale = np.max(np.abs(b), axis=axes, keepdims=b.ndim >= 2)
+        bound = rtol * scale + atol + 0.0 * b
+    else:
+        bound = rtol * np.abs(b) + atol
+    ok = err <= bound
+    ratio = float(np.max(err / np.maximum(bound, 1e-300))) if err.size else 0.0
+    rel = float(np.max(err / np.maximum(bound - atol, 1e-300) * rtol)) if (err.size and rtol > 0) else 0.0
+    print(f"  {what or kind}: max |err| {err.max() if err.size else 0:.2e}, {mode}wise rel err "
+          f"{rel:.2e}, max err/bound {ratio:.3f}")
     if not ok.all():
-        i = np.unravel_index(np.argmax(np.abs(np.asarray(a) - np.asarray(b))), np.shape(a))
+        i = np.unravel_index(np.argmax(err / np.maximum(bound, 1e-300)), np.shape(a))
         raise AssertionError(f"{what}: {int((~ok).sum())} entries off, worst at {i}: "
-                             f"{np.asarray(a)[i]} vs {np.asarray(b)[i]}")
+                             f"{a[i]} vs {b[i]} (bound {bound[i]:.3e}, {mode}wise rtol {rtol}, atol {atol})")
+
+
+def mask128(lo, hi):
+    return [int(np.uint64(l)) | (int(np.uint64(h)) << 64) for l, h in zip(lo, hi)]
 
 
 @pytest.fixture(scope="module")
@@ -72,12 +110,12 @@ def test_c1_step_sequence(torch_cuda):
         assert ok
         assert fl.n_wake == g["n_wake_steps"][t], t
         assert_close(x, g["states"][t + 1], what=f"state step {t}")
-        assert_close(fw, g["fw"][t], rtol=1e-3, what=f"fw step {t}")
+        assert_close(fw, g["fw"][t], "fw", what=f"fw step {t}")
     n = int(g["n_wake"])
     assert fl.n_wake == n == 96
     np.testing.assert_array_equal(fl.wake_age[:n], g["wake_age"][:n])
-    assert_close(fl.wake_pos[:n], g["wake_pos"][:n], what="wake_pos")
-    assert_close(fl.wake_gamma[:n], g["wake_gamma"][:n], rtol=1e-3, what="wake_gamma")
+    assert_close(fl.wake_pos[:n], g["wake_pos"][:n], "wake_pos", what="wake_pos")
+    assert_close(fl.wake_gamma[:n], g["wake_gamma"][:n], "wake_gamma", what="wake_gamma")
 
 
 def test_c1_rollout_and_fluid(torch_cuda):
@@ -111,8 +149,9 @@ def test_fluid_step_matches_oracle(torch_cuda, oracle_core):
         assert rc == 0 and fl_g.n_wake == flat_o[3] and (fl_g.ring_a, fl_g.ring_b) == flat_o[4:6]
         n = fl_g.n_wake
         np.testing.assert_array_equal(fl_g.wake_age[:n], flat_o[2][:n])
-        assert_close(fl_g.wake_pos[:n], flat_o[0][:n], what="pos")
-        assert_close(fw, fw_o, rtol=1e-3, what="fw")
+        assert_close(fl_g.wake_pos[:n], flat_o[0][:n], "wake_pos", what="pos")
+        assert_close(fl_g.wake_gamma[:n], flat_o[1][:n], "wake_gamma", what="gamma")
+        assert_close(fw, fw_o, "fw", what="fw")
         fl = fl_g
         x[0] += 0.07
 
@@ -125,7 +164,7 @@ def test_mppi_C2_golden(torch_cuda):
     mcfg = config.MppiConfig(batch=256, iterations=3, horizon=50)
     u = mppi.optimize(sc["x0"], fluid_from(sc, 60), sc["warm"], mcfg, eng,
                       np.random.default_rng(int(g["seed"])))
-    assert_close(u, g["u_star"], rtol=1e-3, what="u*")
+    assert_close(u, g["u_star"], "u", what="u*")
 
 
 def _device_iteration(torch, sc, K, seed, diagnostics=True):
@@ -154,52 +193,101 @@ def _oracle_iteration(oracle_core, sc, noise):
     return d
 
 
+def _check_decisions(gpu, ref, what):
+    """Discrete decisions exact off near-ties: status, 128-bit shed mask, final wake
+    size and the wake-index signature; returns the clean-and-successful row mask."""
+    near = (ref["gate_margin"] < GATE_DELTA) | (ref["ring_margin"] < RING_DELTA)
+    clean = ~near
+    g_mask = np.array(mask128(gpu["shed_mask"], gpu["shed_mask_hi"]), dtype=object)
+    r_mask = np.array(mask128(ref["shed_mask"], ref["shed_mask_hi"]), dtype=object)
+    g_sig = gpu["wake_hash"].astype(np.uint64)
+    differ = ((gpu["status"] != ref["status"]) | (g_mask != r_mask) | (gpu["n_final"] != ref["n_final"])
+              | (g_sig != ref["wake_hash"]))
+    B = len(ref["status"])
+    print(f"{what}: {int(near.sum())} near-tie rollouts of {B} (margin < {GATE_DELTA:g}; "
+          f"{int((differ & near).sum())} of them decided differently), "
+          f"{int((ref['status'] != 0).sum())} failed, {int(clean.sum())} checked bit-exactly")
+    np.testing.assert_array_equal(gpu["status"][clean], ref["status"][clean])
+    assert (g_mask[clean] == r_mask[clean]).all(), "shed steps differ"
+    np.testing.assert_array_equal(gpu["n_final"][clean], ref["n_final"][clean])
+    np.testing.assert_array_equal(g_sig[clean], ref["wake_hash"][clean])
+    assert not (differ & clean).any()
+    return clean & (ref["status"] == 0)
+
+
 @pytest.mark.parametrize("name,K,seed", [("scenario_C2.npz", 256, 11), ("scenario_C3.npz", 128, 12),
                                          ("scenario_C4.npz", 64, 13)])
 def test_device_batch_vs_oracle_margin_aware(torch_cuda, oracle_core, name, K, seed):
     sc = golden(name)
     _, noise, gpu = _device_iteration(torch_cuda, sc, K, seed)
     ref = _oracle_iteration(oracle_core, sc, noise)
-    near = (ref["gate_margin"] < GATE_DELTA) | (ref["ring_margin"] < RING_DELTA)
-    clean = ~near
-    differ = (gpu["status"] != ref["status"]) | (gpu["shed_mask"].astype(np.uint64) != ref["shed_mask"])
-    print(f"{name}: {int(near.sum())} near-tie rollouts of {K + 1}, "
-          f"{int((differ & near).sum())} of them decided differently")
-    np.testing.assert_array_equal(gpu["status"][clean], ref["status"][clean])
-    np.testing.assert_array_equal(gpu["shed_mask"][clean].astype(np.uint64), ref["shed_mask"][clean])
-    np.testing.assert_array_equal(gpu["n_final"][clean], ref["n_final"][clean])
-    ok = clean & (ref["status"] == 0)
+    ok = _check_decisions(gpu, ref, name)
     assert_close(gpu["finals"][ok], ref["finals"][ok], what="finals")
-    assert_close(gpu["cost"][ok], ref["cost"][ok], what="cost")
-    assert not (differ & clean).any()
+    assert_close(gpu["cost"][ok], ref["cost"][ok], "cost", what="cost")
+
+
+@pytest.mark.parametrize("tag,name", [("c3", "scenario_C3.npz"), ("c4", "scenario_C4.npz"),
+                                      ("c3long", "scenario_C3.npz")])
+def test_wake_signature_vs_reference_golden(torch_cuda, tag, name):
+    """The device kernel's wake-index signature against the one computed from the
+    reference's own Engine.step sequence (tests/golden/wake_sig.npz): C3 / C4 MPPI
+    candidates merging at the cap, and H = 100 rollouts (shed steps past 64)."""
+    torch = torch_cuda
+    from paper_2509_16079_b200.device import DevicePlan
+    g = golden("wake_sig.npz")
+    sc = golden(name)
+    ctrl = g[tag + "_controls"]
+    plan = DevicePlan(sc["iparams"], sc["fparams"])
+    plan.set_fluid(flat_of(sc))
+    dev = torch.device("cuda")
+    out = plan.batch(torch.as_tensor(sc["x0"], device=dev), ctrl.shape[1],
+                     controls=torch.as_tensor(ctrl, device=dev), rows=len(ctrl), diagnostics=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out["status"].cpu().numpy(), g[tag + "_status"])
+    np.testing.assert_array_equal(out["wake_hash"].cpu().numpy().astype(np.uint64), g[tag + "_sig"])
+    assert_close(out["finals"].cpu().numpy(), g[tag + "_finals"], what=f"{tag} finals")
 
 
 @pytest.mark.parametrize("name,K,seed", [("scenario_C3.npz", 1024, 31), ("scenario_C4.npz", 4096, 32)])
 def test_full_iteration_vs_oracle(torch_cuda, oracle_core, name, K, seed):
     """Every candidate of a full C3 / C4 MPPI iteration (the headline batch, K+1
-    rows, H=50, ring) against the FP64 oracle on the same noise: discrete decisions
-    exact on every rollout away from a near-tie, states/costs within RTOL, and the
-    u* of the device update against the oracle's (softmax over FP32-vs-FP64 costs
-    at lambda = 0.05 is near-argmax: stated tolerance 5e-3)."""
+    rows, H=50, ring) on the same noise against
+      * the reference's own compiled core (oracle/_ref, _core.pyx batch_rollout):
+        status, finals, costs;
+      * the FP64 C oracle (pinned to the reference, tests/test_oracle.py), which
+        also records the per-rollout decision diagnostics: status, shed steps,
+        final wake size and wake-index signature exact away from near-ties;
+    and the MPPI update: normalised weights (mppi.py:46-59) within 1e-4 absolute,
+    u* of the device update within 1e-4 relative of the oracle's."""
     import torch
-    from oracle import planner
+    from oracle import planner, refcore
     from paper_2509_16079_b200.device import mppi_combine
     sc = golden(name)
     plan, noise, gpu = _device_iteration(torch, sc, K, seed)
     ref = _oracle_iteration(oracle_core, sc, noise)
-    near = (ref["gate_margin"] < GATE_DELTA) | (ref["ring_margin"] < RING_DELTA)
-    clean = ~near
-    differ = (gpu["status"] != ref["status"]) | (gpu["shed_mask"].astype(np.uint64) != ref["shed_mask"])
-    ok = clean & (ref["status"] == 0)
-    rel = np.abs(gpu["cost"][ok] - ref["cost"][ok]) / np.maximum(1.0, np.abs(ref["cost"][ok]))
-    print(f"{name} K={K}: {int(near.sum())} near-tie rollouts of {K + 1} "
-          f"({int((differ & near).sum())} decided differently), {int((ref['status'] != 0).sum())} failed, "
-          f"max cost rel err {rel.max():.2e}")
-    np.testing.assert_array_equal(gpu["status"][clean], ref["status"][clean])
-    np.testing.assert_array_equal(gpu["shed_mask"][clean].astype(np.uint64), ref["shed_mask"][clean])
-    np.testing.assert_array_equal(gpu["n_final"][clean], ref["n_final"][clean])
-    assert_close(gpu["finals"][ok], ref["finals"][ok], what="finals")
-    assert_close(gpu["cost"][ok], ref["cost"][ok], what="cost")
+    ok = _check_decisions(gpu, ref, f"{name} K={K}")
+    assert_close(gpu["finals"][ok], ref["finals"][ok], what="finals vs oracle")
+    assert_close(gpu["cost"][ok], ref["cost"][ok], "cost", what="cost vs oracle")
+    # the reference's own compiled core on the same candidates
+    rc = refcore.load()
+    assert rc is not None, "oracle/_ref not built (oracle/build_ref.sh)"
+    st_r, fin_r, _ = rc.batch_rollout(np.ascontiguousarray(sc["x0"]), np.ascontiguousarray(ref["cand"]),
+                                      *flat_of(sc), sc["iparams"], sc["fparams"], False, 0)
+    np.testing.assert_array_equal(st_r, ref["status"])  # FP64 vs FP64
+    np.testing.assert_allclose(fin_r, ref["finals"], rtol=1e-9, atol=1e-11)
+    J_r = planner.terminal_costs(fin_r, st_r, [10, 10, 1, 0, 0.2, 0.2, 0.2], [3.5, 0, np.pi / 4, 0, 0.5, -0.5, 0])
+    clean = (ref["gate_margin"] >= GATE_DELTA) & (ref["ring_margin"] >= RING_DELTA)
+    np.testing.assert_array_equal(gpu["status"][clean], st_r[clean])
+    assert_close(gpu["finals"][ok], fin_r[ok], what="finals vs reference core")
+    assert_close(gpu["cost"][ok], J_r[ok], "cost", what="cost vs reference core")
+    # MPPI weights and u*
+    fin = np.isfinite(J_r)
+    def weights(J):
+        w = np.where(np.isfinite(J), np.exp(-(J - J[np.isfinite(J)].min()) / 0.05), 0.0)
+        return w / w.sum()
+    w_g, w_r = weights(gpu["cost"]), weights(J_r)
+    print(f"  weights: effective sample size {1.0 / np.sum(w_r ** 2):.1f}, max weight {w_r.max():.3f}")
+    assert_close(w_g[fin], w_r[fin], "weight", what="normalised weights")
     dev = torch.device("cuda")
     us = torch.as_tensor(np.ascontiguousarray(sc["warm"]), device=dev)
     part = plan.mppi_partial(torch.as_tensor(gpu["cost"], device=dev), us,
@@ -209,10 +297,10 @@ def test_full_iteration_vs_oracle(torch_cuda, oracle_core, name, K, seed):
     mppi_combine(part.view(1, -1), 0.05, new, flag)
     torch.cuda.synchronize()
     assert flag.item() == 0
-    u_ref = planner.weighted_mean(ref["cand"], ref["cost"], 0.05)
     u_gpu = new.cpu().numpy()
-    print(f"  u* max rel err vs oracle {np.max(np.abs(u_gpu - u_ref) / np.maximum(1.0, np.abs(u_ref))):.2e}")
-    assert_close(u_gpu, u_ref, rtol=5e-3, what="u*")
+    np.testing.assert_allclose(u_gpu, planner.weighted_mean(ref["cand"], gpu["cost"], 0.05), rtol=1e-10,
+                               atol=1e-12)
+    assert_close(u_gpu, planner.weighted_mean(ref["cand"], J_r, 0.05), "u", what="u* vs reference core")
 
 
 def test_mppi_update_vs_oracle(torch_cuda, oracle_core):
@@ -238,7 +326,7 @@ def test_mppi_update_vs_oracle(torch_cuda, oracle_core):
     # same costs in -> FP64 update agrees to rounding
     u_same = planner.weighted_mean(ref["cand"], gpu["cost"], 0.05)
     np.testing.assert_allclose(new.cpu().numpy(), u_same, rtol=1e-10, atol=1e-12)
-    assert_close(new.cpu().numpy(), u_ref, rtol=1e-3, what="u*")
+    assert_close(new.cpu().numpy(), u_ref, "u", what="u*")
 
 
 def test_policy_C2_golden(torch_cuda):
@@ -253,7 +341,7 @@ def test_policy_C2_golden(torch_cuda):
     assert_close(states[ok], g["cloud_states"][ok], what="cloud")
     pol = policy.build_policy(nom, fluid_from(sc, 60), config.SynthesisConfig(), eng,
                               np.random.default_rng(int(g["seed"])))
-    assert_close(pol.gains, g["gains"], rtol=2e-2, what="gains")
+    assert_close(pol.gains, g["gains"], "gain", what="gains")
 
 
 def test_policy_kernels_on_reference_cloud(torch_cuda):
@@ -290,13 +378,13 @@ def test_replan_on_device_matches_reference(torch_cuda):
     assert tp == g["proj_t"] and flp.n_wake == int(g["proj_n_wake"])
     assert_close(xp, g["proj_x"], what="projected state")
     np.testing.assert_array_equal(flp.wake_age[: flp.n_wake], g["proj_wake_age"])
-    assert_close(flp.wake_pos[: flp.n_wake], g["proj_wake_pos"], what="projected wake")
+    assert_close(flp.wake_pos[: flp.n_wake], g["proj_wake_pos"], "wake_pos", what="projected wake")
     new = replan.replan(replan.ReplanRequest(x=x0, fluid=fl0, policy=pol, t=0.0, t_proj=10), cfg, eng,
                         np.random.default_rng(1))
     assert new is not None and new.t_start == g["new_t_start"]
-    assert_close(new.nominal.inputs, g["new_inputs"], rtol=1e-3, what="replanned u*")
-    assert_close(new.nominal.states, g["new_states"], rtol=1e-3, what="replanned nominal")
-    assert_close(new.gains, g["new_gains"], rtol=5e-2, what="replanned gains")
+    assert_close(new.nominal.inputs, g["new_inputs"], "u", what="replanned u*")
+    assert_close(new.nominal.states, g["new_states"], "state", what="replanned nominal")
+    assert_close(new.gains, g["new_gains"], "gain", what="replanned gains")
 
 
 def test_replan_leaves_the_generator_where_the_reference_does(torch_cuda):
@@ -344,7 +432,7 @@ def test_c4_full_batch_properties(torch_cuda, oracle_core):
     K = 4096
     plan, noise, a = _device_iteration(torch, sc, K, 5)
     _, _, b = _device_iteration(torch, sc, K, 5)
-    for k in ("status", "finals", "cost", "shed_mask", "n_final"):
+    for k in ("status", "finals", "cost", "shed_mask", "shed_mask_hi", "n_final", "wake_hash"):
         np.testing.assert_array_equal(a[k], b[k])
     assert np.all(a["n_final"] <= 512) and np.all(a["n_final"] >= 500)
     # a 33-row slice computed alone is bitwise identical to the same rows of the full batch
@@ -361,11 +449,9 @@ def test_c4_full_batch_properties(torch_cuda, oracle_core):
     from oracle import planner
     cand = planner.candidates(sc["warm"], noise[0], 2.0, 15.0)[rows]
     d = oracle_core.batch_rollout_diag(sc["x0"], cand, *flat_of(sc), sc["iparams"], sc["fparams"])
-    clean = (d["gate_margin"] >= GATE_DELTA) & (d["ring_margin"] >= RING_DELTA)
-    np.testing.assert_array_equal(a["status"][rows][clean], d["status"][clean])
-    np.testing.assert_array_equal(a["shed_mask"][rows][clean].astype(np.uint64), d["shed_mask"][clean])
-    ok = clean & (d["status"] == 0)
-    assert_close(a["finals"][rows][ok], d["finals"][ok], what="finals")
+    sub_a = {k: v[rows] for k, v in a.items()}
+    ok = _check_decisions(sub_a, d, "C4 random rows")
+    assert_close(sub_a["finals"][ok], d["finals"][ok], what="finals")
 
 
 # ------------------------------------------------------------------ edge cases
@@ -394,7 +480,26 @@ def test_odd_configs_vs_oracle(torch_cuda, oracle_core, nb, cap):
     clean = (d["gate_margin"] >= GATE_DELTA) & (d["ring_margin"] >= RING_DELTA)
     np.testing.assert_array_equal(res.status[clean], d["status"][clean])
     ok = clean & (d["status"] == 0)
-    assert_close(res.trajectories[ok], d["trajs"][ok], rtol=1e-3, what="trajs")
+    # Conditioning: the ring is injected 0.8 m ahead, its cores (r_c = 0.02) sweep
+    # past the plate and small caps merge every step, so the FP64 reference itself
+    # moves by up to ~2e-4 (normwise) when only its INPUTS are rounded at FP32 level
+    # (6e-8).  Tolerance = max(1e-4, 20 x that measured sensitivity) normwise.
+    sens = 0.0
+    for k in range(3):
+        r = np.random.default_rng(100 + k)
+        fp_ = vpm.inject_ring(vpm.FluidState.empty(v), vpm.RingDisturbance.from_speed([0.8, -0.05], 7.5, 0.28,
+                                                                                       0.02, -1.0))
+        n = fp_.n_wake
+        fp_.wake_pos[:n] *= 1.0 + 6e-8 * r.normal(size=(n, 2))
+        d2 = oracle_core.batch_rollout_diag(X0 * (1.0 + 6e-8 * r.normal(size=7)), ctrl, *fp_.flat(), eng.iparams,
+                                            eng.fparams, record=True)
+        m = ok & (d2["status"] == 0)
+        e = np.abs(d2["trajs"][m] - d["trajs"][m]).max(axis=(0, 1)) / np.abs(d["trajs"][m]).max(axis=(0, 1))
+        sens = max(sens, float(e.max()))
+    rtol = max(1e-4, 20.0 * sens)
+    print(f"  nb={nb} cap={cap}: FP64 reference sensitivity to FP32-rounded inputs {sens:.2e} -> rtol {rtol:.2e}")
+    TOL["edge"] = ("norm", rtol, 1e-9)
+    assert_close(res.trajectories[ok], d["trajs"][ok], "edge", what="trajs")
 
 
 def test_overfull_snapshot_and_reversed_flow(torch_cuda, oracle_core):
@@ -418,7 +523,7 @@ def test_overfull_snapshot_and_reversed_flow(torch_cuda, oracle_core):
         d = oracle_core.batch_rollout_diag(x0, ctrl, *fl.flat(), eng.iparams, eng.fparams, record=True)
         np.testing.assert_array_equal(res.status, d["status"])
         ok = d["status"] == 0
-        assert_close(res.trajectories[ok], d["trajs"][ok], rtol=1e-3, what="trajs")
+        assert_close(res.trajectories[ok], d["trajs"][ok], what="trajs")
 
 
 def test_envelope_blowup_status(torch_cuda, oracle_core):
@@ -568,4 +673,4 @@ def test_c5_large_wake_vs_oracle(torch_cuda, oracle_core, N):
     rc_o, _, flat_o = oracle_core.rollout(x0, ctrl[0], *fl.flat(), eng.iparams, eng.fparams, False, True)
     assert rc == rc_o == 0 and fl_g.n_wake == flat_o[3] == N
     np.testing.assert_array_equal(fl_g.wake_age[:N], flat_o[2][:N])
-    assert_close(fl_g.wake_pos[:N], flat_o[0][:N], what=f"C5 N={N} wake")
+    assert_close(fl_g.wake_pos[:N], flat_o[0][:N], "wake_pos", what=f"C5 N={N} wake")

@@ -118,3 +118,41 @@ def test_refcore_agrees_with_oracle_when_built(oracle_core):
                                        g["fparams"], record=True)
     np.testing.assert_array_equal(s, d["status"])
     np.testing.assert_allclose(t, d["trajs"], rtol=1e-9, atol=1e-11)
+
+
+@pytest.mark.parametrize("tag,name", [("c3", "scenario_C3.npz"), ("c4", "scenario_C4.npz"),
+                                      ("c3long", "scenario_C3.npz")])
+def test_wake_signature_matches_reference(oracle_core, tag, name):
+    """The oracle's wake-index signature (per-step wake size / ring indices / shed
+    flag chain + final index->age sum) equals the one computed from the reference's
+    own Engine.step sequence (tests/golden/make_golden.py wake_sig), on MPPI
+    candidates of the C3 / C4 ring scenarios (merging at cap every shed step) and on
+    H=100 rollouts (shed bits past step 64); per-step wake sizes and the shed
+    bitmask agree with it."""
+    g = golden("wake_sig.npz")
+    sc = golden(name)
+    ctrl = g[tag + "_controls"]
+    d = oracle_core.batch_rollout_diag(sc["x0"], ctrl, *flat_of(sc), sc["iparams"], sc["fparams"],
+                                       per_step_n=True)
+    np.testing.assert_array_equal(d["status"], g[tag + "_status"])
+    np.testing.assert_array_equal(d["wake_hash"], g[tag + "_sig"])
+    ns = g[tag + "_n_steps"]
+    np.testing.assert_array_equal(np.where(ns >= 0, d["n_steps"], -1), ns)
+    np.testing.assert_allclose(d["finals"], g[tag + "_finals"], rtol=1e-9, atol=1e-11)
+    T = ctrl.shape[1]
+    bits = [(int(d["shed_mask"][k]) | (int(d["shed_mask_hi"][k]) << 64)) for k in range(len(ctrl))]
+    assert any(b >> 64 for b in bits) or T <= 64
+    assert all(b < (1 << T) for b in bits)
+
+
+def test_wake_signature_sensitive_to_order(oracle_core):
+    """The signature is a real check: it changes when two final ages swap places
+    or a step's merge count moves to another step."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from wake_sig import signature
+    steps = [(10, -1, -1, True), (10, -1, -1, False)]
+    a = signature(steps, [3, 2, 1])
+    assert a != signature(steps, [2, 3, 1])
+    assert a != signature([(12, -1, -1, True), (10, -1, -1, False)], [3, 2, 1])
+    assert a != signature([(10, 4, 5, True), (10, -1, -1, False)], [3, 2, 1])
