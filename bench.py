@@ -138,22 +138,23 @@ def time_cpu_sample(core, sc, flat, noise, rows):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(sc, flat, target_s=12.0):
+def cpu_baseline(sc, flat):
+    """The reference's CPU planner on one full C4 iteration (all 4097 candidate rows,
+    same snapshot and noise shape as the GPU arm), all host threads."""
     core, kind = reference_core()
     noise = np.random.default_rng(1234).normal(0.0, 1.0, (K_SAMPLES, HORIZON))
     threads = os.cpu_count() or 1
-    probe = max(2, min(K_SAMPLES + 1, threads * 2))
-    dt = time_cpu_sample(core, sc, flat, noise, probe)
-    rows = int(min(K_SAMPLES + 1, max(probe, probe * target_s / max(dt, 1e-6))))
-    rows = max(threads, (rows // threads) * threads) if rows < K_SAMPLES + 1 else rows
-    dt = time_cpu_sample(core, sc, flat, noise, rows)
-    return {"value": rows / dt, "unit": "rollouts/s", "cores": threads, "kind": kind,
-            "sample": f"{rows} of the {K_SAMPLES + 1} C4 candidate rollouts (H=50, N=512 + ring), "
-                      f"FP64, {threads} OpenMP threads, {dt:.1f} s; full iteration would take "
-                      f"{(K_SAMPLES + 1) / (rows / dt):.1f} s"}
+    time_cpu_sample(core, sc, flat, noise, 2 * threads)  # warm the OpenMP pool
+    dt = time_cpu_sample(core, sc, flat, noise, K_SAMPLES + 1)
+    return {"value": (K_SAMPLES + 1) / dt, "unit": "rollouts/s", "cores": threads, "kind": kind,
+            "sample": f"one full C4 MPPI iteration: all {K_SAMPLES + 1} candidate rollouts (H=50, N=512 + "
+                      f"ring) + terminal costs + softmax update, FP64, {threads} OpenMP threads, {dt:.2f} s"}
 
 
 def run_reference(args):
+    """--impl reference: the reference's own compiled CPU core (oracle/_ref), full C4
+    iterations (4097 rollouts + costs + update) per timed step -- no extrapolation.
+    Warm-up steps run a small slice (OpenMP pool and page cache only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -161,24 +162,94 @@ def run_reference(args):
     core, kind = reference_core()
     noise = np.random.default_rng(1234).normal(0.0, 1.0, (K_SAMPLES, HORIZON))
     threads = os.cpu_count() or 1
-    rows = max(threads * 2, 16)
     for _ in range(max(args.warmup, 1)):
-        dt = time_cpu_sample(core, sc, flat, noise, rows)
-    # size each timed step at about 4 s so --steps K --warmup W stays within minutes
-    rows = int(min(K_SAMPLES + 1, max(rows, rows * 4.0 / max(dt, 1e-6))))
-    times = [time_cpu_sample(core, sc, flat, noise, rows) for _ in range(args.steps)]
+        time_cpu_sample(core, sc, flat, noise, 2 * threads)
+    times = [time_cpu_sample(core, sc, flat, noise, K_SAMPLES + 1) for _ in range(args.steps)]
     tot = sum(times)
-    value = rows * args.steps / tot
+    value = (K_SAMPLES + 1) * args.steps / tot
     line = {"metric": METRIC, "value": value, "unit": "rollouts/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * (K_SAMPLES + 1) / value, "higher_is_better": True,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": CONFIG,
             "cpu_baseline": {"value": value, "unit": "rollouts/s", "cores": threads, "kind": kind,
-                             "sample": f"{rows} of {K_SAMPLES + 1} C4 rollouts per step"},
+                             "sample": f"full C4 iterations ({K_SAMPLES + 1} rollouts each), "
+                                       f"{args.steps} timed, {min(times):.2f}-{max(times):.2f} s each"},
             "e2e": {"value": value, "unit": "rollouts/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def cpu_baselines_other_configs():
+    """Same-run CPU baselines for the other BASELINE.json configs, on the reference's
+    compiled core (oracle/_ref, all host threads) -- C2 and C3 as full iterations,
+    C5 on a K-subset extrapolated linearly in K (labelled) -- and, past the compiled
+    core's MAXW = 1028 (C5 N = 2048), the reference's numpy induced_velocity_at
+    (vpm.py:105-128) on a K-subset, extrapolated."""
+    from oracle import planner
+    core, kind = reference_core()
+    threads = os.cpu_count() or 1
+    out = {"cores": threads, "kind": kind}
+    for tag, name, K in (("C2", "scenario_C2.npz", 256), ("C3", "scenario_C3.npz", 1024)):
+        with np.load(os.path.join(ROOT, "tests", "golden", name)) as z:
+            s = {k: z[k] for k in z.files}
+        fl = (s["wake_pos"], s["wake_gamma"], s["wake_age"], int(s["n_wake"]), int(s["ring_a"]), int(s["ring_b"]),
+              s["prev_pos"], s["prev_gamma"], int(s["n_prev"]), float(s["prev_lev"]), s["ema"])
+        cand = np.ascontiguousarray(planner.candidates(np.full(HORIZON, -6.0),
+                                                       np.random.default_rng(7).normal(0, 1, (K, HORIZON)),
+                                                       SIGMA, 15.0))
+        core.batch_rollout(s["x0"], cand[: 2 * threads], *fl, s["iparams"], s["fparams"], False, threads)
+        t0 = time.perf_counter()
+        st, fin, _ = core.batch_rollout(s["x0"], cand, *fl, s["iparams"], s["fparams"], False, threads)
+        planner.weighted_mean(cand, planner.terminal_costs(fin, st, Q, XPERCH), LAMBDA)
+        dt = time.perf_counter() - t0
+        out[tag] = {"iteration_ms": 1e3 * dt, "rollouts_per_s": (K + 1) / dt,
+                    "sample": f"full iteration, {K + 1} rollouts"}
+    from paper_2509_16079_b200 import config
+    c5 = {}
+    K5, H5 = 16384, 5
+    for N in (128, 256, 512, 1024, 2048):
+        rng = np.random.default_rng(11)
+        v = config.VpmConfig(particle_cap=N)
+        ip, fp = config.pack_params(v, config.GliderParams())
+        wp = rng.normal(0.0, 0.5, (N, 2))
+        wp[:, 0] -= 3.0
+        g = rng.normal(0.0, 0.05, N)
+        inter = N * (N - 1) + 10 * N * 3  # wake-wake + bound row + collocation + loads (no shedding)
+        if N <= 1024:
+            fl = (wp, g, np.zeros(N, np.int64), N, -1, -1, np.zeros((10, 2)), np.zeros(10), 0, 0.0, np.zeros(10))
+            x0 = np.array([0.0, 0.0, 0.0, 0.0, 7.0, 0.0, 0.0])
+            sub = max(threads, min(K5, int(2e9 / (N * N * H5))))  # ~1-2 s of work
+            sub = (sub // threads) * threads
+            ctrl = np.zeros((sub, H5))
+            core.batch_rollout(x0, ctrl[:threads], *fl, ip, fp, False, threads)
+            t0 = time.perf_counter()
+            core.batch_rollout(x0, ctrl, *fl, ip, fp, False, threads)
+            dt = time.perf_counter() - t0
+            c5[str(N)] = {"ms_extrapolated_K16384": 1e3 * dt * K5 / sub, "sample_rollouts": sub,
+                          "gflops": 12.0 * inter * H5 * sub / dt / 1e9,
+                          "sample": f"{sub} of {K5} rollouts x {H5} steps on the compiled core, "
+                                    "extrapolated linearly in K"}
+        else:
+            from oracle import refpkg
+            if not refpkg.available():
+                c5[str(N)] = {"unavailable": "reference package not staged (oracle/build_ref.sh)"}
+                continue
+            refpkg.load()
+            import importlib
+            vpm_ref = importlib.import_module("perchsim.vpm")
+            reps = 3
+            t0 = time.perf_counter()
+            for _ in range(reps):  # one rollout-step's wake-wake sum, the O(N^2) part
+                vpm_ref.induced_velocity_at(wp, wp, g, vpm_ref.KERNEL_REGULARIZED, 0.02)
+            dt = (time.perf_counter() - t0) / reps
+            c5[str(N)] = {"ms_extrapolated_K16384": 1e3 * dt * K5 * H5, "sample_rollout_steps": reps,
+                          "gflops": 12.0 * N * N / dt / 1e9,
+                          "sample": "numpy induced_velocity_at (vpm.py:105-128) of one 2048-particle wake "
+                                    "on itself, 1 thread, extrapolated to K=16384 x H=5 (compiled core "
+                                    "limited to N <= 1024 by MAXW)"}
+    out["C5"] = {"K": K5, "H": H5, "by_N": c5}
+    return out
 
 
 # ------------------------------------------------------------------------------ GPU arm
@@ -217,6 +288,22 @@ def extras(torch, dev, sc, flat, plan, mp):
     x2 = f64(s2["x0"])
     out["c2_iteration_ms"] = _time_ms(torch, lambda: p2.mppi_iteration(
         x2, u2, n2, SIGMA, 257, LAMBDA, f64(Q), f64(XPERCH), sc2))
+    # C3: K=1024 (+1), H=50, N<=256 + ring (reference-generated prefilled wake)
+    with np.load(os.path.join(ROOT, "tests", "golden", "scenario_C3.npz")) as z:
+        s3 = {k: z[k] for k in z.files}
+    p3 = DevicePlan(s3["iparams"], s3["fparams"], device=dev.index)
+    p3.set_fluid((s3["wake_pos"], s3["wake_gamma"], s3["wake_age"], int(s3["n_wake"]), int(s3["ring_a"]),
+                  int(s3["ring_b"]), s3["prev_pos"], s3["prev_gamma"], int(s3["n_prev"]), float(s3["prev_lev"]),
+                  s3["ema"]))
+    n3 = f64(np.random.default_rng(6).normal(0, 1, (1024, HORIZON)))
+    sc3 = {"cost": torch.empty(1025, dtype=torch.float64, device=dev),
+           "partial": torch.empty(HORIZON + 2, dtype=torch.float64, device=dev),
+           "flag": torch.zeros(1, dtype=torch.int32, device=dev)}
+    u3 = f64(np.full(HORIZON, -6.0))
+    ms3 = _time_ms(torch, lambda: p3.mppi_iteration(f64(s3["x0"]), u3, n3, SIGMA, 1025, LAMBDA, f64(Q),
+                                                     f64(XPERCH), sc3))
+    out["c3_iteration"] = {"ms": ms3, "rollouts_per_s": 1025 / (ms3 * 1e-3),
+                           "config": "C3: K=1024 (+incumbent), H=50, N<=256 + ring, 1 GPU"}
     # policy synthesis (64 perturbed rollouts on the N=512 + ring snapshot, regression,
     # Riccati) through the C ABI with host buffers, around the current u*
     cfg = config.ExperimentConfig()
@@ -508,8 +595,9 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "rollouts/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": dict(CONFIG, parallelism=f"rollout rows sharded over {world} GPU(s), "
-                                           "1 all_gather of W x (H+2) f64 per iteration"),
+        "config": CONFIG,
+        "parallelism": f"rollout rows sharded over {world} GPU(s), 1 all_gather of W x (H+2) f64 per "
+                       "iteration" if world > 1 else "1 GPU: rollout rows in one launch, no collective",
         "latency_ms": ms_per_step,
         "biot_savart_gflops": 12.0 * inter_all / (kern_ms_max * 1e-3) / 1e9 if kern_ms_max > 0 else None,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -535,6 +623,8 @@ def run_ours(args):
         line["extras"] = extras(torch, dev, sc, flat, plan, mp)
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(sc, flat)
+        if "extras" in line:
+            line["extras"]["cpu_baselines"] = cpu_baselines_other_configs()
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

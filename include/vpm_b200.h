@@ -176,7 +176,9 @@ int vpm_mppi_partial(vpm_plan *p, const double *d_cost, int rows, int row_begin,
                      double temperature, double *d_partial, void *stream);
 
 /* Combine W gathered partials (W, H+2) in rank order into d_ustar (H).  Sets
- * *d_flag = 1 when every candidate failed (the caller raises). */
+ * *d_flag = 1 when every candidate failed (d_ustar untouched; the caller raises).
+ * The flag is sticky: the kernel never clears it, callers zero it once per
+ * optimisation, so a failed iteration is never masked by a later success. */
 int vpm_mppi_combine(const double *d_partials, int W, int T, double temperature,
                      double *d_ustar, int32_t *d_flag, void *stream);
 
@@ -189,8 +191,9 @@ int vpm_mppi_combine(const double *d_partials, int W, int T, double temperature,
 int vpm_noise_philox(uint64_t seed, uint64_t iteration, int row_begin, int rows, int T,
                      double *d_out, void *stream);
 
-/* Whole MPPI iteration on one device (batch + partial + combine), optionally
- * replayed from a CUDA graph captured on first use (use_graph != 0).
+/* Whole MPPI iteration on one device (batch + partial + combine): three kernel
+ * launches on stream.  use_graph is reserved and ignored (callers that want graph
+ * replay capture the stream themselves, as replan.py does).
  * d_noise: (B_total - 1, T).  d_cost scratch (B_total) and d_partial (T+2). */
 int vpm_mppi_iteration(vpm_plan *p, const double *d_x0, double *d_ustar, const double *d_noise,
                        double sigma, int B_total, int T, double temperature, const double *d_q,

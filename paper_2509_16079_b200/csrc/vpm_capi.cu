@@ -278,6 +278,13 @@ cudaError_t launch_r(const Args &a, int grid, const Shape &sh, size_t smem, cuda
 cudaError_t launch_rollouts(Args a, int grid, cudaStream_t st) {
   const Shape sh = pick_shape(a.P.cap, a.P.nb, grid);
   const size_t smem = vpm::make_layout(a.P.cap, a.P.nb, sh.nt).total;
+#ifdef VPM_TUNING_SUBSET
+  // tuning builds (tools/): only the shapes the C4 / 8-GPU-shard / C2 launches pick
+  if (sh.r == 5 && sh.minb == 72) return launch_t<5, 72>(a, grid, sh.nt, smem, st);
+  if (sh.r == 3 && sh.minb == 64) return launch_t<3, 64>(a, grid, sh.nt, smem, st);
+  if (sh.r == 1 && sh.minb == 64) return launch_t<1, 64>(a, grid, sh.nt, smem, st);
+  return cudaErrorNotSupported;
+#else
   switch (sh.minb) {
     case 48: return launch_r<48>(a, grid, sh, smem, st);
     case 56: return launch_r<56>(a, grid, sh, smem, st);
@@ -285,6 +292,7 @@ cudaError_t launch_rollouts(Args a, int grid, cudaStream_t st) {
     case 80: return launch_r<80>(a, grid, sh, smem, st);
     default: return launch_r<64>(a, grid, sh, smem, st);
   }
+#endif
 }
 
 int check_fluid(const vpm_fluid *f, const Phys &P) {
@@ -657,7 +665,7 @@ int vpm_mppi_iteration(vpm_plan *p, const double *d_x0, double *d_ustar, const d
                        double sigma, int B_total, int T, double temperature, const double *d_q,
                        const double *d_xperch, double *d_cost, double *d_partial, int32_t *d_flag,
                        int use_graph, void *stream) {
-  (void)use_graph;  // one persistent CTA per rollout already amortises the H steps
+  (void)use_graph;  // reserved (vpm_b200.h); stream capture is the caller's choice
   vpm_batch_out o;
   std::memset(&o, 0, sizeof(o));
   o.cost = d_cost;

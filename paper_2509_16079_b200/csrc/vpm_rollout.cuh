@@ -1228,7 +1228,9 @@ __global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
   }
 }
 
-// Combine W gathered partials in rank order.
+// Combine W gathered partials in rank order.  The failure flag is
+// sticky: set to 1 when every candidate failed (u* left unchanged), never cleared
+// here -- callers zero it when an optimisation starts.
 __global__ void mppi_combine_kernel(const double *__restrict__ parts, int W, int T, double lambda,
                                     double *__restrict__ ustar, int32_t *__restrict__ flag) {
   const int ld = T + 2;
@@ -1251,7 +1253,6 @@ __global__ void mppi_combine_kernel(const double *__restrict__ parts, int W, int
     }
     ustar[t] = S / Z;
   }
-  if (threadIdx.x == 0 && flag) *flag = 0;
 }
 
 // ---- device noise (performance mode) ----------------------------------

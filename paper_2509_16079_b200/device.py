@@ -34,10 +34,25 @@ def _p(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
-def _stream(stream=None):
+def _stream(stream=None, device=None):
+    """The launch stream: ``stream`` if given, else torch's current stream OF THE
+    DEVICE the buffers live on (not of whatever device is current)."""
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return C.c_void_p(s.cuda_stream)
+
+
+def _on(t):
+    """Device guard for the plan-less entry points: kernels launch on the current
+    device, so make it the device of ``t``."""
+    return _torch().cuda.device(t.device)
+
+
+def _need_f64(t, name, dim=None):
+    torch = _torch()
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and (dim is None or t.dim() == dim)):
+        raise ValueError(f"{name} must be a contiguous CUDA float64 tensor"
+                         + (f" of {dim} dimensions" if dim else ""))
 
 
 class DevicePlan:
@@ -118,7 +133,7 @@ class DevicePlan:
         check(_lib.lib().vpm_plan_batch(
             self.handle, _p(x0), stride, _p(controls), _p(ustar), _p(noise), float(sigma),
             int(row_begin), int(row_begin + rows), int(T), _p(q), _p(x_perch), int(bool(record)),
-            C.byref(bo), _stream(stream)), "plan_batch")
+            C.byref(bo), _stream(stream, self.device)), "plan_batch")
         return o
 
     # ---- MPPI update ----------------------------------------------------------------
@@ -130,7 +145,7 @@ class DevicePlan:
             partial = torch.empty(T + 2, dtype=torch.float64, device=cost.device)
         check(_lib.lib().vpm_mppi_partial(
             self.handle, _p(cost), int(cost.shape[0]), int(row_begin), _p(ustar), _p(noise),
-            float(sigma), T, float(temperature), _p(partial), _stream(stream)), "mppi_partial")
+            float(sigma), T, float(temperature), _p(partial), _stream(stream, self.device)), "mppi_partial")
         return partial
 
     def mppi_iteration(self, x0, ustar, noise, sigma: float, B_total: int, temperature: float,
@@ -140,7 +155,7 @@ class DevicePlan:
         check(_lib.lib().vpm_mppi_iteration(
             self.handle, _p(x0), _p(ustar), _p(noise), float(sigma), int(B_total), T,
             float(temperature), _p(q), _p(x_perch), _p(scratch["cost"]), _p(scratch["partial"]),
-            _p(scratch["flag"]), 0, _stream(stream)), "mppi_iteration")
+            _p(scratch["flag"]), 0, _stream(stream, self.device)), "mppi_iteration")
 
     # ---- replan pieces ------------------------------------------------------------------
     def project(self, x0, T: int, gains, states, inputs, t_start: float, t0: float,
@@ -153,7 +168,7 @@ class DevicePlan:
         check(_lib.lib().vpm_plan_project(
             self.handle, _p(x0), int(T), _p(gains), _p(states), _p(inputs), int(gains.shape[0]),
             float(t_start), float(t0), _p(status), _p(final), int(bool(write_snapshot)),
-            _stream(stream)), "plan_project")
+            _stream(stream, self.device)), "plan_project")
         return status, final
 
     def cloud(self, x0, x0_noise, x0_scale, ustar, u_noise, sigma_u: float, stream=None):
@@ -164,7 +179,7 @@ class DevicePlan:
         trajs = torch.zeros(K, T + 1, 7, dtype=torch.float64, device=x0.device)
         check(_lib.lib().vpm_plan_cloud(
             self.handle, _p(x0), _p(x0_noise), _p(x0_scale), _p(ustar), _p(u_noise), float(sigma_u),
-            K, T, _p(status), _p(trajs), _stream(stream)), "plan_cloud")
+            K, T, _p(status), _p(trajs), _stream(stream, self.device)), "plan_cloud")
         return status, trajs
 
     def download_fluid(self):
@@ -187,17 +202,22 @@ class DevicePlan:
 def mppi_combine(partials, temperature: float, ustar, flag=None, stream=None):
     """Combine (W, T+2) gathered shard partials in rank order into ``ustar``."""
     W, ld = int(partials.shape[0]), int(partials.shape[1])
-    check(_lib.lib().vpm_mppi_combine(_p(partials), W, ld - 2, float(temperature), _p(ustar),
-                                      _p(flag), _stream(stream)), "mppi_combine")
+    _need_f64(partials, "partials", 2)
+    _need_f64(ustar, "ustar", 1)
+    with _on(ustar):
+        check(_lib.lib().vpm_mppi_combine(_p(partials), W, ld - 2, float(temperature), _p(ustar),
+                                          _p(flag), _stream(stream, ustar.device)), "mppi_combine")
 
 
 def noise_philox(seed: int, iteration: int, out, row_begin: int = 0, stream=None):
     """Fill the CUDA float64 tensor ``out`` (rows, T) with rows [row_begin, row_begin
     + rows) of iteration ``iteration``'s device-drawn standard-normal noise
     (``vpm_noise_philox``: counter-based Philox keyed by (seed, iteration, row))."""
+    _need_f64(out, "out", 2)  # the kernel writes rows x T doubles with row stride T
     rows, T = int(out.shape[0]), int(out.shape[1])
-    check(_lib.lib().vpm_noise_philox(int(seed) & (2**64 - 1), int(iteration), int(row_begin), rows, T,
-                                      _p(out), _stream(stream)), "noise_philox")
+    with _on(out):
+        check(_lib.lib().vpm_noise_philox(int(seed) & (2**64 - 1), int(iteration), int(row_begin), rows, T,
+                                          _p(out), _stream(stream, out.device)), "noise_philox")
     return out
 
 
@@ -211,11 +231,18 @@ def policy_fit(nom_x, nom_u, cloud_x, cloud_u, status, dt: float, q_running, r_r
     z = lambda *s: torch.zeros(*s, dtype=torch.float64, device=dev)
     ac, bc, ad, bd, g = z(H, 3, 5), z(H, 3), z(H, 7, 7), z(H, 7), z(H, 7)
     flag = torch.zeros(4, dtype=torch.int32, device=dev)
+    with _on(nom_x):
+        _policy_fit_call(nom_x, nom_u, cloud_x, cloud_u, status, K, H, dt, q_running, r_running, q_final,
+                         ac, bc, ad, bd, g, flag, stream)
+    return ac, bc, ad, bd, g, flag
+
+
+def _policy_fit_call(nom_x, nom_u, cloud_x, cloud_u, status, K, H, dt, q_running, r_running, q_final,
+                     ac, bc, ad, bd, g, flag, stream):
     check(_lib.lib().vpm_policy_fit(
         _p(nom_x), _p(nom_u), _p(cloud_x), _p(cloud_u), _p(status), K, H, float(dt), _p(q_running),
         float(r_running), _p(q_final), _p(ac), _p(bc), _p(ad), _p(bd), _p(g), _p(flag), 1, 1,
-        _stream(stream)), "policy_fit")
-    return ac, bc, ad, bd, g, flag
+        _stream(stream, nom_x.device)), "policy_fit")
 
 
 def launch_shape(cap: int, nb: int, rows: int):

@@ -77,6 +77,10 @@ class ShardedMppi:
         self.partial = torch.empty(self.T + 2, **f64)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
 
+    def reset(self) -> None:
+        """Start a new optimisation: clear the sticky all-candidates-failed flag."""
+        self.flag.zero_()
+
     def set_noise(self, noise_rows):
         self.noise = noise_rows
 
@@ -98,10 +102,18 @@ class ShardedMppi:
         self.plan.mppi_partial(self.out["cost"], self.ustar, self.noise, self.sigma,
                                self.temperature, row_begin=self.begin, partial=self.partial,
                                stream=stream)
-        parts = self.partial.view(1, -1) if self.world == 1 else gather_partials(self.partial, self.group)
+        # world 1 without an explicit group: no collective at all; with a group (any
+        # size, e.g. a world-1 NCCL group in tests) the partials go through it
+        if self.world == 1 and self.group is None:
+            parts = self.partial.view(1, -1)
+        else:
+            parts = gather_partials(self.partial, self.group)
         mppi_combine(parts, self.temperature, self.ustar, self.flag, stream=stream)
 
     def check(self) -> None:
+        """Raise like mppi.py:55-56 if any iteration since the last reset() had every
+        candidate fail (the combine kernel's flag is sticky; a later successful
+        iteration does not clear it)."""
         if int(self.flag.item()) != 0:
             raise ValueError("all sampled rollouts failed (infinite cost)")
 

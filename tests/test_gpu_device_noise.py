@@ -110,6 +110,26 @@ def test_replan_with_device_noise(torch_cuda):
     assert np.isfinite(a.gains).all() and np.abs(a.nominal.inputs).max() <= cfg.glider.u_limit
     c = rp.replan(req, cfg, eng, dn)  # next counter block: a different plan
     assert c is None or not np.array_equal(c.nominal.inputs, a.nominal.inputs)
+    # wiring: the same draws fed through the host path (iterations MPPI blocks, then
+    # the cloud's start perturbations dx0 (k, 7) -- scaled by state_stdev -- and
+    # input perturbations du (k, H) -- scaled by input_stdev) give bitwise the same
+    # policy as the device-drawn replan
+    import torch
+    from paper_2509_16079_b200.device import noise_philox
+    K, iters, k = cfg.mppi.batch, cfg.mppi.iterations, cfg.synthesis.n_samples
+    H = len(a.nominal.inputs)
+    draw = lambda i, r, c: noise_philox(9, i, torch.empty((r, c), dtype=torch.float64, device="cuda")).cpu().numpy()
+    blocks = [draw(i, K, H) for i in range(iters)] + [draw(iters, k, 7), draw(iters + 1, k, H)]
+    rep = _Replay(blocks)
+    h = rp.replan(req, cfg, eng, rep)
+    assert h is not None and not rep.blocks  # every block consumed, in order
+    np.testing.assert_array_equal(h.gains, a.gains)
+    np.testing.assert_array_equal(h.nominal.inputs, a.nominal.inputs)
+    np.testing.assert_array_equal(h.nominal.states, a.nominal.states)
+    # a swapped wiring (dx0 <-> du roles) would not reproduce it
+    bad = [draw(i, K, H) for i in range(iters)] + [draw(iters + 1, k, 7), draw(iters, k, H)]
+    w = rp.replan(req, cfg, eng, _Replay(bad))
+    assert w is None or not np.array_equal(w.gains, a.gains)
 
 
 def test_bootstrap_with_device_noise(torch_cuda):

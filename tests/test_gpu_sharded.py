@@ -123,3 +123,70 @@ def test_two_process_ranks_agree():
     plan, x0, warm, noise, qq, xp = _setup(torch, torch.device("cuda", 0))
     u2, _ = _sharded_ustar(torch, plan, x0, warm, noise, qq, xp, 2)
     np.testing.assert_array_equal(res[0], u2)
+
+
+def test_failure_flag_is_sticky():
+    """An all-candidates-failed iteration is not masked by a later successful one
+    (ADVICE r1): check() raises until reset()."""
+    import torch
+    from paper_2509_16079_b200.sharding import ShardedMppi
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    plan, x0, warm, noise, q, xp = _setup(torch, dev)
+    bad = x0.clone()
+    bad[6] = 400.0  # leaves the envelope on the first step: every candidate fails
+    mp_ = ShardedMppi(plan, bad, warm, noise, B=K + 1, sigma=SIGMA, temperature=LAM, q=q, x_perch=xp)
+    mp_.iteration()
+    mp_.x0 = x0
+    mp_.iteration()
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError):
+        mp_.check()
+    mp_.reset()
+    mp_.iteration()
+    mp_.check()
+
+
+def _nccl_rank(port, out_q):
+    try:
+        import sys
+        import torch
+        import torch.distributed as dist
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), NCCL_DEBUG="INFO")
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        from paper_2509_16079_b200.sharding import ShardedMppi
+        plan, x0, warm, noise, q, xp = _setup(torch, dev)
+        mp_ = ShardedMppi(plan, x0, warm, noise, B=K + 1, sigma=SIGMA, temperature=LAM, q=q, x_perch=xp,
+                          rank=0, world=1, group=dist.group.WORLD)
+        assert dist.get_backend(mp_.group) == "nccl"
+        mp_.iteration()  # rollouts + partial + NCCL all_gather_into_tensor + combine
+        torch.cuda.synchronize()
+        mp_.check()
+        out_q.put(("ok", mp_.ustar.cpu().numpy(), torch.cuda.nccl.version()))
+        dist.destroy_process_group()
+    except Exception as err:
+        out_q.put(("err", repr(err), None))
+
+
+def test_nccl_world1_all_gather_path():
+    """The NCCL branch of gather_partials (all_gather_into_tensor) executed: a world-1
+    NCCL process group on cuda:0 runs ShardedMppi.iteration through the collective;
+    u* equals the no-collective single-GPU iteration bitwise."""
+    import torch
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_rank, args=(_free_port(), q))
+    p.start()
+    status, u, ver = q.get(timeout=300)
+    p.join(timeout=120)
+    assert status == "ok", u
+    print("NCCL", ver)
+    torch.cuda.set_device(0)
+    plan, x0, warm, noise, qq, xp = _setup(torch, torch.device("cuda", 0))
+    u1, _ = _sharded_ustar(torch, plan, x0, warm, noise, qq, xp, 1)
+    np.testing.assert_array_equal(u, u1)

@@ -63,6 +63,29 @@ def test_worker_rejected_replan_is_reported(monkeypatch):
     assert w.poll(0.3) == (None, True)
 
 
+def test_worker_failure_is_raised_not_a_stale_policy(monkeypatch):
+    """A replan that raises in the threaded worker must surface from poll(), never
+    hand back the previous cycle's policy as a fresh replan."""
+    results = iter([("policy", 0.0)])
+
+    def flaky(req, cfg, engine, rng):
+        try:
+            return next(results)
+        except StopIteration:
+            raise FloatingPointError("device failure") from None
+
+    monkeypatch.setattr(nmpc, "replan", flaky)
+    w = nmpc._WorkerHandle(None, _FakeEngine(), None, threaded=True)
+    w.request(_request(0.0))
+    w.join()
+    assert w.poll(0.1) == (("policy", 0.0), True)
+    w.request(_request(0.1))
+    w.join()
+    with pytest.raises(RuntimeError, match="replanning worker failed"):
+        w.poll(0.2)
+    assert w.status == w.READY
+
+
 def test_pressure_trigger_empty_wake_never_fires():
     from paper_2509_16079_b200.vpm import FluidState
     fl = FluidState.empty(ExperimentConfig().vpm)
