@@ -385,10 +385,78 @@ def extras(torch, dev, sc, flat, plan, mp):
                          "gflops": 12.0 * inter / (ms * 1e-3) / 1e9,
                          "frac_of_fp32_peak": 12.0 * inter / (ms * 1e-3) / 1e12 / FP32_SPEC_TFLOPS,
                          "failed_rollouts": shed}
+    out["single_instance_stepping"] = step_latency(torch)
     out["c5_biot_savart_sweep"] = {"K": K5, "H": H5, "by_N": sweep,
                                    "note": "random wake pos~N(0,0.5^2), Gamma~N(0,0.05^2), "
                                            "attached flow; 12 flop per directed interaction"}
     return out
+
+
+def step_latency(torch):
+    """Single-instance stepping (rollout.py:81-98, called every tick at nmpc.py:314-315):
+    per-call latency of Engine.step / fluid_step through the reference stepping
+    contract with host buffers (the C ABI's vpm_step), of the device-resident step
+    (plant.DeviceWake: x up, a small record back, the fluid stays on the device),
+    of one resident control-loop tick (plant step + sensor + observed-wake step, one
+    sync), and of the reference's compiled core step on this host (oracle/_ref,
+    FP64, 1 thread per call) -- at cap 60 (the closed-loop default, ~60-particle
+    wake) and cap 512 (the C4 N=512 + ring snapshot)."""
+    from paper_2509_16079_b200 import config, rollout, vpm
+    from paper_2509_16079_b200.plant import DeviceWake
+    core, kind = reference_core()
+    x0 = np.array([0.0, 0.0, 0.3, 0.0, 7.0, 0.0, 0.0])
+    res = {"reference_kind": kind}
+    for cap in (60, 512):
+        cfg = config.ExperimentConfig()
+        cfg.vpm.particle_cap = cap
+        eng = rollout.Engine(cfg.vpm, cfg.glider)
+        if cap == 512:
+            sc, _ = load_scenario()
+            fl = vpm.FluidState.empty(cfg.vpm)
+            n = int(sc["n_wake"])
+            fl.wake_pos[:n], fl.wake_gamma[:n], fl.wake_age[:n] = sc["wake_pos"][:n], sc["wake_gamma"][:n], sc["wake_age"][:n]
+            fl.n_wake, fl.ring_a, fl.ring_b = n, int(sc["ring_a"]), int(sc["ring_b"])
+            fl.prev_pos[:], fl.prev_gamma[:], fl.n_prev = sc["prev_pos"], sc["prev_gamma"], int(sc["n_prev"])
+            fl.prev_lev_gamma, fl.unsteady_ema[:] = float(sc["prev_lev"]), sc["ema"]
+        else:
+            fl, xx = vpm.FluidState.empty(cfg.vpm), x0.copy()
+            for _ in range(40):  # prefill to the cap through the plant itself
+                _, xx, fl, _ = eng.step(xx, -15.0, fl)
+        reps = 200
+
+        def timed(fn):
+            for _ in range(10):
+                fn()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                fn()
+            return 1e6 * (time.perf_counter() - t0) / reps
+
+        r = {"n_wake": int(fl.n_wake)}
+        r["engine_step_us"] = timed(lambda: eng.step(x0, -6.0, fl))
+        r["engine_fluid_step_us"] = timed(lambda: eng.fluid_step(x0, fl))
+        dw = DeviceWake(eng, fl)
+        ob = DeviceWake(eng, fl)
+
+        def resident_step():
+            dw.step_async(x0, -6.0, True)
+            dw.sync()
+            return dw.record()
+
+        def resident_tick():
+            dw.step_async(x0, -6.0, True, sensor=(1.0, 0.3), r_core=cfg.vpm.r_core)
+            ob.step_async(x0, 0.0, False)
+            dw.sync()
+            ob.sync()
+            return dw.record(), ob.record()
+
+        r["resident_step_us"] = timed(resident_step)
+        r["resident_loop_tick_us"] = timed(resident_tick)
+        ip, fp = eng.iparams, eng.fparams
+        flat = fl.flat()
+        r["reference_core_step_us"] = timed(lambda: core.step(x0, -6.0, *flat, ip, fp, True))
+        res[f"cap{cap}"] = r
+    return res
 
 
 def c5_sharded(torch, dev, rank, world):

@@ -156,6 +156,28 @@ int vpm_plan_project(vpm_plan *p, const double *d_x0, int T, const double *d_gai
                      double t0, int64_t *d_status, double *d_final, int write_snapshot,
                      void *stream);
 
+/* Device-resident single step: Engine.step (integrate=1) / Engine.fluid_step
+ * (integrate=0) of rollout.py:81-98 (_core.pyx:536-576) on the plan's snapshot IN
+ * PLACE -- the stepped fluid becomes the snapshot, no host round trip of the wake.
+ * x (7, host) and u are passed by value; with sensor (host xz) the FP64 induced
+ * velocity there (vpm.py:93-128, regularised, r_core) is evaluated on the stepped
+ * wake (the NMPC pressure sensor, nmpc.py:73-85).  Queues the launch(es) and ONE
+ * copy of the step record into h_record (pinned host, VPM_STEP_RECORD_BYTES):
+ *   double x[7] (new state), fw[3] {fw_x, fw_z, m_w}, q[2] (sensor velocity);
+ *   int32 rc (0 ok, 2 non-finite), n_wake, ring_a, ring_b, n_prev.
+ * Returns without synchronising (vpm_stream_sync).  The plant / observed-wake loop
+ * of nmpc.py:314-315 keeps its two fluids on the device between ticks this way. */
+#define VPM_STEP_RECORD_BYTES 128
+int vpm_plan_step(vpm_plan *p, const double *x, double u, int integrate, const double *sensor,
+                  double r_core, void *h_record, void *stream);
+
+/* Induced velocity (FP64, regularised with r_core) at one host point from the
+ * plan's current device wake, synchronous.  out (2). */
+int vpm_plan_probe(vpm_plan *p, const double *target, double r_core, double *out);
+
+/* cudaStreamSynchronize on a stream passed as void*. */
+int vpm_stream_sync(void *stream);
+
 /* Perturbed cloud (perturbed_rollouts, policy.py:66-91) in one launch: row r starts
  * at x0 + x0_noise[r] * x0_scale and applies clip(u* + u_noise[r] * sigma_u);
  * trajectories (rows, T+1, 7) recorded. */

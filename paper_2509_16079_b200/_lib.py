@@ -137,6 +137,9 @@ def lib():
             "vpm_plan_cloud": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_double, C.c_int, C.c_int, vp,
                                          vp, vp]),
             "vpm_plan_download_fluid": (C.c_int, [vp, C.POINTER(VpmFluidOut)]),
+            "vpm_plan_step": (C.c_int, [vp, _D, C.c_double, C.c_int, _D, C.c_double, vp, vp]),
+            "vpm_plan_probe": (C.c_int, [vp, _D, C.c_double, _D]),
+            "vpm_stream_sync": (C.c_int, [vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -152,7 +155,8 @@ EXPORTED = ("vpm_step", "vpm_rollout", "vpm_batch_rollout", "vpm_batch_rollout_x
             "vpm_mppi_optimize_host", "vpm_plan_timing", "vpm_fp32_peak_probe", "vpm_launch_shape",
             "vpm_boundary_inverse", "vpm_policy_fit", "vpm_build_policy_host",
             "vpm_policy_fit_host", "vpm_tvlqr_host", "vpm_plan_project", "vpm_plan_cloud",
-            "vpm_plan_download_fluid", "vpm_induced_velocity_host")
+            "vpm_plan_download_fluid", "vpm_induced_velocity_host", "vpm_plan_step", "vpm_plan_probe",
+            "vpm_stream_sync")
 
 
 def last_error() -> str:

@@ -327,6 +327,7 @@ struct vpm_plan {
   double *d_wbuf = nullptr;  // chunk partials of the MPPI softmax reduction
   size_t wbuf_len = 0;
   unsigned *d_ticket = nullptr;  // last-CTA ticket of the chunked reduction (re-armed by it)
+  void *d_rec = nullptr;         // single-step record (vpm_plan_step)
   // rollout-kernel timing
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // start/stop pairs
@@ -455,18 +456,22 @@ void vpm_plan_destroy(vpm_plan *p) {
   if (p->h_snap) cudaFreeHost(p->h_snap);
   cudaFree(p->d_wbuf);
   cudaFree(p->d_ticket);
+  cudaFree(p->d_rec);
   cudaFree(p->hscratch);
   if (p->hstream) cudaStreamDestroy(p->hstream);
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
   delete p;
 }
 
-int vpm_plan_set_fluid(vpm_plan *p, const vpm_fluid *f) {
+// Upload a snapshot.  st == nullptr: synchronous, after every launch of every stream
+// (the public entry point).  st != nullptr: queued on st behind the launches already
+// there -- for a plan used on that one stream only (the thread-local host plans).
+static int set_fluid_on(vpm_plan *p, const vpm_fluid *f, cudaStream_t st) {
   if (!p) return fail_cfg("null plan");
   int rc = check_fluid(f, p->P);
   if (rc) return rc;
   CK(cudaSetDevice(p->device));
-  CK(cudaDeviceSynchronize());  // no launch of any stream may still read the old snapshot
+  if (!st) CK(cudaDeviceSynchronize());  // no launch of any stream may still read the old snapshot
   // pack the used parts into the pinned mirror at their device offsets, one copy up
   const int cap4 = p->P.cap + 4, nb = p->P.nb;
   double *h = p->h_snap;
@@ -483,7 +488,8 @@ int vpm_plan_set_fluid(vpm_plan *p, const vpm_fluid *f) {
   h[4 * cap4 + 4 * nb] = f->prev_lev;
   const int32_t scal[4] = {f->n_wake, f->ring_a, f->ring_b, f->n_prev};
   std::memcpy(h + 4 * cap4 + 4 * nb + 1, scal, sizeof(scal));
-  CK(cudaMemcpy(p->d_snap, h, sizeof(double) * p->snap_doubles, cudaMemcpyHostToDevice));
+  if (st) CK(cudaMemcpyAsync(p->d_snap, h, sizeof(double) * p->snap_doubles, cudaMemcpyHostToDevice, st));
+  else CK(cudaMemcpy(p->d_snap, h, sizeof(double) * p->snap_doubles, cudaMemcpyHostToDevice));
   p->n_wake = f->n_wake;
   p->ring_a = f->ring_a;
   p->ring_b = f->ring_b;
@@ -491,6 +497,8 @@ int vpm_plan_set_fluid(vpm_plan *p, const vpm_fluid *f) {
   p->prev_lev = f->prev_lev;
   return VPM_OK;
 }
+
+int vpm_plan_set_fluid(vpm_plan *p, const vpm_fluid *f) { return set_fluid_on(p, f, nullptr); }
 
 int vpm_plan_batch(vpm_plan *p, const double *d_x0, int x0_stride, const double *d_controls,
                    const double *d_ustar, const double *d_noise, double sigma, int row_begin,
@@ -563,6 +571,75 @@ int vpm_plan_project(vpm_plan *p, const double *d_x0, int T, const double *d_gai
   std::lock_guard<std::mutex> lk(p->mu);
   CK(cudaSetDevice(p->device));
   return plan_launch(p, a, 1, (cudaStream_t)stream);
+}
+
+// Device record of the single-step path: one D2H copy per call (vpm_b200.h).
+struct StepRecord {
+  double x[7], fw[3], q[2];
+  int32_t rc, scal[4], pad[3];
+};
+static_assert(sizeof(StepRecord) == VPM_STEP_RECORD_BYTES, "record layout");
+
+int vpm_plan_step(vpm_plan *p, const double *x, double u, int integrate, const double *sensor,
+                  double r_core, void *h_record, void *stream) {
+  if (!p || !x) return fail_cfg("null plan / state");
+  std::lock_guard<std::mutex> lk(p->mu);
+  CK(cudaSetDevice(p->device));
+  if (!p->d_rec) CK(cudaMalloc(&p->d_rec, sizeof(StepRecord)));
+  StepRecord *r = (StepRecord *)p->d_rec;
+  Args a = base_args(p);
+  a.use_x0v = 1;
+  std::memcpy(a.x0v, x, sizeof(a.x0v));
+  a.T = 1;
+  a.rows = 1;
+  a.integrate = integrate;
+  a.check_envelope = 0;  // Engine.step semantics: rc only (rollout.py:81-86, _core.pyx:536-576)
+  a.use_u_const = 1;
+  a.u_const = u;
+  a.finals = r->x;
+  a.rc_out = &r->rc;
+  a.fw_out = r->fw;
+  a.need_fluid = 1;      // the stepped fluid replaces the plan's snapshot in place
+  a.o_wpos = p->d_wpos;
+  a.o_wgam = p->d_wgam;
+  a.o_wage = p->d_wage;
+  a.o_scal = p->d_scal;
+  a.o_ppos = p->d_ppos;
+  a.o_pgam = p->d_pgam;
+  a.o_plev = p->d_plev;
+  a.o_ema = p->d_ema;
+  a.o_scal2 = r->scal;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = plan_launch(p, a, 1, st);
+  if (rc) return rc;
+  if (sensor) {
+    const double rc2 = r_core * r_core;
+    vpm::induced_velocity1_kernel<<<1, 32, 0, st>>>(p->d_wpos, p->d_wgam, p->d_scal, sensor[0], sensor[1],
+                                                    rc2 * rc2, 0, r->q);
+    CK(cudaGetLastError());
+  }
+  if (h_record) CK(cudaMemcpyAsync(h_record, r, sizeof(StepRecord), cudaMemcpyDeviceToHost, st));
+  return VPM_OK;
+}
+
+int vpm_plan_probe(vpm_plan *p, const double *target, double r_core, double *out) {
+  if (!p || !target || !out) return fail_cfg("null plan / target / output");
+  std::lock_guard<std::mutex> lk(p->mu);
+  CK(cudaSetDevice(p->device));
+  CK(cudaDeviceSynchronize());  // the snapshot may still be written by a queued step
+  if (!p->d_rec) CK(cudaMalloc(&p->d_rec, sizeof(StepRecord)));
+  StepRecord *r = (StepRecord *)p->d_rec;
+  const double rc2 = r_core * r_core;
+  vpm::induced_velocity1_kernel<<<1, 32>>>(p->d_wpos, p->d_wgam, p->d_scal, target[0], target[1], rc2 * rc2, 0,
+                                           r->q);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out, r->q, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+  return VPM_OK;
+}
+
+int vpm_stream_sync(void *stream) {
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return VPM_OK;
 }
 
 int vpm_plan_cloud(vpm_plan *p, const double *d_x0, const double *d_x0_noise,
@@ -825,8 +902,24 @@ struct HostCtx {
   cudaStream_t st = nullptr;
   void *scratch = nullptr;
   size_t scratch_len = 0;
+  char *pin = nullptr;  // pinned staging of the packed small outputs (one D2H per call)
+  size_t pin_len = 0;
 };
 thread_local HostCtx g_host;
+
+char *host_pinned(size_t bytes) {
+  HostCtx &h = g_host;
+  if (h.pin_len < bytes) {
+    if (h.pin) cudaFreeHost(h.pin);
+    h.pin = nullptr;
+    if (cudaMallocHost(&h.pin, bytes) != cudaSuccess) {
+      h.pin_len = 0;
+      return nullptr;
+    }
+    h.pin_len = bytes;
+  }
+  return h.pin;
+}
 
 int host_plan(const int64_t *ip, const double *fp, vpm_plan **out, cudaStream_t *st) {
   HostCtx &h = g_host;
@@ -873,7 +966,11 @@ struct Carve {
   }
 };
 
-// Shared driver for step / rollout / batch_rollout with host buffers.
+// Shared driver for step / rollout / batch_rollout with host buffers.  Everything is
+// queued on the thread's own stream (the snapshot upload too: the thread-local plan
+// is used on that stream only), the small outputs -- status, rc, finals, loads and
+// the returned fluid -- are carved contiguously on the device and come back in ONE
+// copy through pinned staging; the stream is synchronised once.
 int host_run(const double *x0, int x0_stride, const double *controls, int B, int T,
              const vpm_fluid *fluid, const int64_t *ip, const double *fp, int integrate,
              int check_env, int record, int64_t *status, double *finals, double *trajs,
@@ -886,25 +983,43 @@ int host_run(const double *x0, int x0_stride, const double *controls, int B, int
   cudaStream_t st;
   rc = host_plan(ip, fp, &p, &st);
   if (rc) return rc;
-  rc = vpm_plan_set_fluid(p, fluid);
+  rc = set_fluid_on(p, fluid, st);
   if (rc) return rc;
-  if (B == 0) return VPM_OK;
+  if (B == 0) {
+    CK(cudaStreamSynchronize(st));
+    return VPM_OK;
+  }
   const int cap4 = P.cap + 4, nb = P.nb;
   const size_t ntraj = record ? (size_t)B * (T + 1) * 7 : 0;
-  const size_t need = 256 * 16 + sizeof(double) * ((size_t)B * 7 + (size_t)B * T + (size_t)B * 7 + ntraj + 3 * (size_t)B +
+  const size_t need = 256 * 20 + sizeof(double) * ((size_t)B * 7 + (size_t)B * T + (size_t)B * 7 + ntraj + 3 * (size_t)B +
                                                    3 * cap4 + 4 * nb + 1) +
                       sizeof(int64_t) * ((size_t)B + cap4) + sizeof(int32_t) * ((size_t)B + 4);
   void *sc = host_scratch(need);
   if (!sc) return fail_cfg("device scratch allocation failed");
   Carve cv{(char *)sc};
-  double *d_x0 = cv.take<double>((size_t)(x0_stride ? B : 1) * 7);
-  double *d_ctrl = cv.take<double>((size_t)B * (T > 0 ? T : 1));
-  double *d_fin = cv.take<double>((size_t)B * 7);
-  double *d_traj = record ? cv.take<double>(ntraj) : nullptr;
-  double *d_fw = cv.take<double>((size_t)B * 3);
+  // packed small outputs first (one D2H), then the trajectories, then the inputs
   int64_t *d_st = cv.take<int64_t>(B);
   int32_t *d_rc = cv.take<int32_t>(B);
+  double *d_fin = cv.take<double>((size_t)B * 7);
+  double *d_fw = cv.take<double>((size_t)B * 3);
   Args a = base_args(p);
+  if (fo) {
+    a.need_fluid = 1;
+    a.o_wpos = cv.take<double>(2 * (size_t)cap4);
+    a.o_wgam = cv.take<double>(cap4);
+    a.o_wage = cv.take<int64_t>(cap4);
+    a.o_scal = cv.take<int32_t>(4);
+    a.o_ppos = cv.take<double>(2 * (size_t)nb);
+    a.o_pgam = cv.take<double>(nb);
+    a.o_plev = cv.take<double>(1);
+    a.o_ema = cv.take<double>(nb);
+  }
+  const size_t small_bytes = cv.off;
+  double *d_traj = record ? cv.take<double>(ntraj) : nullptr;
+  double *d_x0 = cv.take<double>((size_t)(x0_stride ? B : 1) * 7);
+  double *d_ctrl = cv.take<double>((size_t)B * (T > 0 ? T : 1));
+  char *pin = host_pinned(small_bytes);
+  if (!pin) return fail_cfg("pinned staging allocation failed");
   a.x0 = d_x0;
   a.x0_stride = x0_stride;
   a.controls = d_ctrl;
@@ -918,38 +1033,29 @@ int host_run(const double *x0, int x0_stride, const double *controls, int B, int
   a.trajs = d_traj;
   a.rc_out = d_rc;
   a.fw_out = d_fw;
-  if (fo) {
-    a.need_fluid = 1;
-    a.o_wpos = cv.take<double>(2 * (size_t)cap4);
-    a.o_wgam = cv.take<double>(cap4);
-    a.o_wage = cv.take<int64_t>(cap4);
-    a.o_scal = cv.take<int32_t>(4);
-    a.o_ppos = cv.take<double>(2 * (size_t)nb);
-    a.o_pgam = cv.take<double>(nb);
-    a.o_plev = cv.take<double>(1);
-    a.o_ema = cv.take<double>(nb);
-  }
   CK(cudaMemcpyAsync(d_x0, x0, sizeof(double) * (x0_stride ? B : 1) * 7, cudaMemcpyHostToDevice, st));
   if (T > 0) CK(cudaMemcpyAsync(d_ctrl, controls, sizeof(double) * (size_t)B * T, cudaMemcpyHostToDevice, st));
   if (record) CK(cudaMemsetAsync(d_traj, 0, sizeof(double) * ntraj, st));
   rc = plan_launch(p, a, B, st);
   if (rc) return rc;
-  if (status) CK(cudaMemcpyAsync(status, d_st, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, st));
-  if (rc_out) CK(cudaMemcpyAsync(rc_out, d_rc, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
-  if (finals) CK(cudaMemcpyAsync(finals, d_fin, sizeof(double) * B * 7, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(pin, sc, small_bytes, cudaMemcpyDeviceToHost, st));
   if (trajs && record) CK(cudaMemcpyAsync(trajs, d_traj, sizeof(double) * ntraj, cudaMemcpyDeviceToHost, st));
-  if (fw_out) CK(cudaMemcpyAsync(fw_out, d_fw, sizeof(double) * 3, cudaMemcpyDeviceToHost, st));
-  if (fo) {
-    CK(cudaMemcpyAsync(fo->wake_pos, a.o_wpos, sizeof(double) * 2 * cap4, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(fo->wake_gamma, a.o_wgam, sizeof(double) * cap4, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(fo->wake_age, a.o_wage, sizeof(int64_t) * cap4, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(fo->scalars, a.o_scal, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(fo->prev_pos, a.o_ppos, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(fo->prev_gamma, a.o_pgam, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(fo->prev_lev, a.o_plev, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(fo->ema, a.o_ema, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
-  }
   CK(cudaStreamSynchronize(st));
+  auto from = [&](const void *d) { return pin + ((const char *)d - (const char *)sc); };
+  if (status) std::memcpy(status, from(d_st), sizeof(int64_t) * B);
+  if (rc_out) std::memcpy(rc_out, from(d_rc), sizeof(int32_t) * B);
+  if (finals) std::memcpy(finals, from(d_fin), sizeof(double) * B * 7);
+  if (fw_out) std::memcpy(fw_out, from(d_fw), sizeof(double) * 3);
+  if (fo) {
+    std::memcpy(fo->wake_pos, from(a.o_wpos), sizeof(double) * 2 * cap4);
+    std::memcpy(fo->wake_gamma, from(a.o_wgam), sizeof(double) * cap4);
+    std::memcpy(fo->wake_age, from(a.o_wage), sizeof(int64_t) * cap4);
+    std::memcpy(fo->scalars, from(a.o_scal), sizeof(int32_t) * 4);
+    std::memcpy(fo->prev_pos, from(a.o_ppos), sizeof(double) * 2 * nb);
+    std::memcpy(fo->prev_gamma, from(a.o_pgam), sizeof(double) * nb);
+    std::memcpy(fo->prev_lev, from(a.o_plev), sizeof(double));
+    std::memcpy(fo->ema, from(a.o_ema), sizeof(double) * nb);
+  }
   return VPM_OK;
 }
 

@@ -155,6 +155,11 @@ struct Args {
   const double *pol_gains, *pol_states, *pol_inputs;
   int pol_h;
   double pol_t_start, pol_t0;
+  // single-step mode (vpm_plan_step): start state and control by value
+  double u_const;
+  int use_u_const;
+  double x0v[7];
+  int use_x0v;
   int T, row_begin, rows;
   int integrate, check_envelope, need_fluid, record;
   // outputs (any may be null)
@@ -172,6 +177,7 @@ struct Args {
   int64_t *o_wage;
   int32_t *o_scal;
   double *o_ppos, *o_pgam, *o_plev, *o_ema;
+  int32_t *o_scal2;  // optional second copy of the dumped scalars (single-step mode)
 };
 
 struct Ctl {
@@ -435,7 +441,9 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
 __device__ __forceinline__ double control_at(const Args &a, int row, int t, const double *x,
                                              double tacc) {
   double u;
-  if (a.pol_gains) {
+  if (a.use_u_const) {
+    u = a.u_const;
+  } else if (a.pol_gains) {
     // evaluate_policy (policy.py:236-244): Python round() is round-half-even = rint
     int k = (int)rint((tacc - a.pol_t_start) * a.P.inv_dt);
     k = k < 0 ? 0 : (k > a.pol_h - 1 ? a.pol_h - 1 : k);
@@ -499,7 +507,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
       pzp[j] = have ? a.ppos[2 * j + 1] : 0.0;
       ema[j] = a.ema[j];
     }
-    const double *x0 = a.x0 + (size_t)row * a.x0_stride;
+    const double *x0 = a.use_x0v ? a.x0v : a.x0 + (size_t)row * a.x0_stride;
     if (lane < 7) {
       double xv = x0[lane];
       if (a.x0_noise) xv += a.x0_noise[(size_t)row * 7 + lane] * a.x0_scale[lane];
@@ -1090,6 +1098,12 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
       a.o_scal[2] = ctl->ring_b;
       a.o_scal[3] = ctl->n_prev;
       a.o_plev[0] = ctl->lev_prev;
+      if (a.o_scal2) {
+        a.o_scal2[0] = nl;
+        a.o_scal2[1] = ctl->ring_a;
+        a.o_scal2[2] = ctl->ring_b;
+        a.o_scal2[3] = ctl->n_prev;
+      }
     }
   }
 }
@@ -1535,6 +1549,32 @@ __global__ void induced_velocity_kernel(const double *__restrict__ pos, const do
   if (lane == 0) {
     out[2 * i] = ux;
     out[2 * i + 1] = uz;
+  }
+}
+
+// One target, source count from the device (a plan's snapshot): the sensor
+// velocity of vpm_plan_step / vpm_plan_probe.  Same per-lane order and butterfly
+// as induced_velocity_kernel, so both give the same bits.
+__global__ void induced_velocity1_kernel(const double *__restrict__ pos, const double *__restrict__ gam,
+                                         const int32_t *__restrict__ n_dev, double tx, double tz,
+                                         double rc4, int singular, double *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int n = n_dev[0];
+  double ux = 0.0, uz = 0.0;
+  for (int j = lane; j < n; j += 32) {
+    const double dx = tx - pos[2 * j], dz = tz - pos[2 * j + 1];
+    const double r2 = dx * dx + dz * dz;
+    double c;
+    if (singular) c = r2 == 0.0 ? 0.0 : gam[j] / (TWO_PI * r2);
+    else c = gam[j] / (TWO_PI * sqrt(r2 * r2 + rc4));
+    ux += c * dz;
+    uz -= c * dx;
+  }
+  ux = warp_sum_d(ux);
+  uz = warp_sum_d(uz);
+  if (lane == 0) {
+    out[0] = ux;
+    out[1] = uz;
   }
 }
 

@@ -295,6 +295,22 @@ def test_trials_reproduce_the_reference_executive():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["no_disturbance", "uncompensated", "compensated"])
+def test_resident_loop_equals_host_stepping(mode):
+    """The control loop with both fluids kept on the device (vpm_plan_step in place,
+    one sync per tick) is bitwise the loop that steps through the reference's
+    host-buffer contract (Engine.step / fluid_step every tick)."""
+    cfg = ExperimentConfig()
+    a = nmpc.control_loop(cfg, mode, 3, resident=True)
+    b = nmpc.control_loop(cfg, mode, 3, resident=False)
+    np.testing.assert_array_equal(a.states, b.states)
+    np.testing.assert_array_equal(a.inputs, b.inputs)
+    np.testing.assert_array_equal(a.wake_counts, b.wake_counts)
+    assert a.trigger_time == b.trigger_time and a.failure == b.failure
+    assert [e.accepted for e in a.replans] == [e.accepted for e in b.replans]
+
+
+@pytest.mark.gpu
 def test_initial_condition_sweep():
     """SPEC run_sweep (Fig. 'ic-sweep'): v_x swept about the nominal 7 m/s; the
     nominal point is included; TVLQR feedback is reported beside the open loop."""
