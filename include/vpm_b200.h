@@ -117,6 +117,12 @@ void vpm_plan_destroy(vpm_plan *p);
 /* Upload the fluid snapshot (host) that every rollout forks from. */
 int vpm_plan_set_fluid(vpm_plan *p, const vpm_fluid *fluid);
 
+/* The two halves of vpm_plan_set_fluid: pack the snapshot into the plan's pinned
+ * mirror (after the device is idle), and queue the mirror's copy to the device on
+ * a stream -- so a captured CUDA graph can contain the upload (replan.py). */
+int vpm_plan_stage_fluid(vpm_plan *p, const vpm_fluid *fluid);
+int vpm_plan_upload_fluid(vpm_plan *p, void *stream);
+
 /* Per-rollout outputs of a device batch; any pointer may be NULL. */
 typedef struct vpm_batch_out {
   int64_t *status;      /* (rows) */
@@ -155,6 +161,12 @@ int vpm_plan_project(vpm_plan *p, const double *d_x0, int T, const double *d_gai
                      const double *d_states, const double *d_inputs, int pol_h, double t_start,
                      double t0, int64_t *d_status, double *d_final, int write_snapshot,
                      void *stream);
+
+/* vpm_plan_project with {t_start, t0} read from device memory d_times (2) at run
+ * time -- for CUDA-graph replay, where by-value arguments are frozen at capture. */
+int vpm_plan_project_dev(vpm_plan *p, const double *d_x0, int T, const double *d_gains,
+                         const double *d_states, const double *d_inputs, int pol_h, const double *d_times,
+                         int64_t *d_status, double *d_final, int write_snapshot, void *stream);
 
 /* Device-resident single step: Engine.step (integrate=1) / Engine.fluid_step
  * (integrate=0) of rollout.py:81-98 (_core.pyx:536-576) on the plan's snapshot IN
@@ -212,6 +224,11 @@ int vpm_mppi_combine(const double *d_partials, int W, int T, double temperature,
  * keeps host-drawn numpy noise (mppi.py:42). */
 int vpm_noise_philox(uint64_t seed, uint64_t iteration, int row_begin, int rows, int T,
                      double *d_out, void *stream);
+
+/* vpm_noise_philox with {seed, iteration} read from device memory d_seed_iter (2)
+ * at run time, iteration + offset used (CUDA-graph replay of a replan cycle). */
+int vpm_noise_philox_dev(const uint64_t *d_seed_iter, uint64_t offset, int row_begin, int rows, int T,
+                         double *d_out, void *stream);
 
 /* Whole MPPI iteration on one device (batch + partial + combine): three kernel
  * launches on stream.  use_graph is reserved and ignored (callers that want graph

@@ -140,6 +140,10 @@ def lib():
             "vpm_plan_step": (C.c_int, [vp, _D, C.c_double, C.c_int, _D, C.c_double, vp, vp]),
             "vpm_plan_probe": (C.c_int, [vp, _D, C.c_double, _D]),
             "vpm_stream_sync": (C.c_int, [vp]),
+            "vpm_plan_stage_fluid": (C.c_int, [vp, C.POINTER(VpmFluid)]),
+            "vpm_plan_upload_fluid": (C.c_int, [vp, vp]),
+            "vpm_plan_project_dev": (C.c_int, [vp, vp, C.c_int, vp, vp, vp, C.c_int, vp, vp, vp, C.c_int, vp]),
+            "vpm_noise_philox_dev": (C.c_int, [vp, C.c_uint64, C.c_int, C.c_int, C.c_int, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -156,7 +160,8 @@ EXPORTED = ("vpm_step", "vpm_rollout", "vpm_batch_rollout", "vpm_batch_rollout_x
             "vpm_boundary_inverse", "vpm_policy_fit", "vpm_build_policy_host",
             "vpm_policy_fit_host", "vpm_tvlqr_host", "vpm_plan_project", "vpm_plan_cloud",
             "vpm_plan_download_fluid", "vpm_induced_velocity_host", "vpm_plan_step", "vpm_plan_probe",
-            "vpm_stream_sync")
+            "vpm_stream_sync", "vpm_plan_project_dev", "vpm_noise_philox_dev",
+            "vpm_plan_stage_fluid", "vpm_plan_upload_fluid")
 
 
 def last_error() -> str:

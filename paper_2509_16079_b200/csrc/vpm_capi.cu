@@ -471,7 +471,9 @@ static int set_fluid_on(vpm_plan *p, const vpm_fluid *f, cudaStream_t st) {
   int rc = check_fluid(f, p->P);
   if (rc) return rc;
   CK(cudaSetDevice(p->device));
-  if (!st) CK(cudaDeviceSynchronize());  // no launch of any stream may still read the old snapshot
+  // synchronous / staging: no launch of any stream may still read the old snapshot
+  // (nor, when staging, the pinned mirror the graph's upload copies from)
+  if (!st || st == reinterpret_cast<cudaStream_t>(uintptr_t(-1))) CK(cudaDeviceSynchronize());
   // pack the used parts into the pinned mirror at their device offsets, one copy up
   const int cap4 = p->P.cap + 4, nb = p->P.nb;
   double *h = p->h_snap;
@@ -488,8 +490,13 @@ static int set_fluid_on(vpm_plan *p, const vpm_fluid *f, cudaStream_t st) {
   h[4 * cap4 + 4 * nb] = f->prev_lev;
   const int32_t scal[4] = {f->n_wake, f->ring_a, f->ring_b, f->n_prev};
   std::memcpy(h + 4 * cap4 + 4 * nb + 1, scal, sizeof(scal));
-  if (st) CK(cudaMemcpyAsync(p->d_snap, h, sizeof(double) * p->snap_doubles, cudaMemcpyHostToDevice, st));
-  else CK(cudaMemcpy(p->d_snap, h, sizeof(double) * p->snap_doubles, cudaMemcpyHostToDevice));
+  if (st == reinterpret_cast<cudaStream_t>(uintptr_t(-1))) {
+    // stage only: the caller uploads (vpm_plan_upload_fluid)
+  } else if (st) {
+    CK(cudaMemcpyAsync(p->d_snap, h, sizeof(double) * p->snap_doubles, cudaMemcpyHostToDevice, st));
+  } else {
+    CK(cudaMemcpy(p->d_snap, h, sizeof(double) * p->snap_doubles, cudaMemcpyHostToDevice));
+  }
   p->n_wake = f->n_wake;
   p->ring_a = f->ring_a;
   p->ring_b = f->ring_b;
@@ -499,6 +506,20 @@ static int set_fluid_on(vpm_plan *p, const vpm_fluid *f, cudaStream_t st) {
 }
 
 int vpm_plan_set_fluid(vpm_plan *p, const vpm_fluid *f) { return set_fluid_on(p, f, nullptr); }
+
+// Pack a snapshot into the plan's pinned mirror only (no copy) / copy the mirror up
+// on a stream: the two halves of set_fluid, so a CUDA graph can contain the upload.
+int vpm_plan_stage_fluid(vpm_plan *p, const vpm_fluid *f) {
+  return set_fluid_on(p, f, reinterpret_cast<cudaStream_t>(uintptr_t(-1)));
+}
+
+int vpm_plan_upload_fluid(vpm_plan *p, void *stream) {
+  if (!p) return fail_cfg("null plan");
+  CK(cudaSetDevice(p->device));
+  CK(cudaMemcpyAsync(p->d_snap, p->h_snap, sizeof(double) * p->snap_doubles, cudaMemcpyHostToDevice,
+                     (cudaStream_t)stream));
+  return VPM_OK;
+}
 
 int vpm_plan_batch(vpm_plan *p, const double *d_x0, int x0_stride, const double *d_controls,
                    const double *d_ustar, const double *d_noise, double sigma, int row_begin,
@@ -536,10 +557,31 @@ int vpm_plan_batch(vpm_plan *p, const double *d_x0, int x0_stride, const double 
   return plan_launch(p, a, a.rows, (cudaStream_t)stream);
 }
 
+static int project_launch(vpm_plan *p, const double *d_x0, int T, const double *d_gains,
+                          const double *d_states, const double *d_inputs, int pol_h, double t_start,
+                          double t0, const double *d_times, int64_t *d_status, double *d_final,
+                          int write_snapshot, void *stream);
+
 int vpm_plan_project(vpm_plan *p, const double *d_x0, int T, const double *d_gains,
                      const double *d_states, const double *d_inputs, int pol_h, double t_start,
                      double t0, int64_t *d_status, double *d_final, int write_snapshot,
                      void *stream) {
+  return project_launch(p, d_x0, T, d_gains, d_states, d_inputs, pol_h, t_start, t0, nullptr, d_status,
+                        d_final, write_snapshot, stream);
+}
+
+int vpm_plan_project_dev(vpm_plan *p, const double *d_x0, int T, const double *d_gains,
+                         const double *d_states, const double *d_inputs, int pol_h, const double *d_times,
+                         int64_t *d_status, double *d_final, int write_snapshot, void *stream) {
+  if (!d_times) return fail_cfg("times pointer must not be null");
+  return project_launch(p, d_x0, T, d_gains, d_states, d_inputs, pol_h, 0.0, 0.0, d_times, d_status, d_final,
+                        write_snapshot, stream);
+}
+
+static int project_launch(vpm_plan *p, const double *d_x0, int T, const double *d_gains,
+                          const double *d_states, const double *d_inputs, int pol_h, double t_start,
+                          double t0, const double *d_times, int64_t *d_status, double *d_final,
+                          int write_snapshot, void *stream) {
   if (!p) return fail_cfg("null plan");
   if (T < 0 || pol_h < 1) return fail_cfg("bad projection horizon / policy length");
   Args a = base_args(p);
@@ -553,6 +595,7 @@ int vpm_plan_project(vpm_plan *p, const double *d_x0, int T, const double *d_gai
   a.pol_h = pol_h;
   a.pol_t_start = t_start;
   a.pol_t0 = t0;
+  a.pol_times = d_times;
   a.status = d_status;
   a.finals = d_final;
   if (write_snapshot) {
@@ -725,17 +768,29 @@ int vpm_mppi_combine(const double *d_partials, int W, int T, double temperature,
   return VPM_OK;
 }
 
-int vpm_noise_philox(uint64_t seed, uint64_t iteration, int row_begin, int rows, int T, double *d_out,
-                     void *stream) {
+static int philox_launch(uint64_t seed, uint64_t iteration, const uint64_t *d_seed_iter, int row_begin,
+                         int rows, int T, double *d_out, void *stream) {
   if (row_begin < 0 || rows < 0 || T < 0) return fail_cfg("bad noise shape");
   if (rows == 0 || T == 0) return VPM_OK;
   if (!d_out) return fail_cfg("noise output must not be null");
   const long long n = (long long)rows * ((T + 1) / 2);
   const int bs = 256;
   vpm::noise_philox_kernel<<<(unsigned)((n + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>(
-      (unsigned long long)seed, (unsigned long long)iteration, row_begin, rows, T, d_out);
+      (unsigned long long)seed, (unsigned long long)iteration, row_begin, rows, T, d_out,
+      (const unsigned long long *)d_seed_iter);
   CK(cudaGetLastError());
   return VPM_OK;
+}
+
+int vpm_noise_philox(uint64_t seed, uint64_t iteration, int row_begin, int rows, int T, double *d_out,
+                     void *stream) {
+  return philox_launch(seed, iteration, nullptr, row_begin, rows, T, d_out, stream);
+}
+
+int vpm_noise_philox_dev(const uint64_t *d_seed_iter, uint64_t offset, int row_begin, int rows, int T,
+                         double *d_out, void *stream) {
+  if (!d_seed_iter) return fail_cfg("seed/iteration pointer must not be null");
+  return philox_launch(0, offset, d_seed_iter, row_begin, rows, T, d_out, stream);
 }
 
 int vpm_mppi_iteration(vpm_plan *p, const double *d_x0, double *d_ustar, const double *d_noise,

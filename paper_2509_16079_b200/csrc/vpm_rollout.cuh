@@ -155,6 +155,7 @@ struct Args {
   const double *pol_gains, *pol_states, *pol_inputs;
   int pol_h;
   double pol_t_start, pol_t0;
+  const double *pol_times;  // optional device {t_start, t0} (graph replay) overriding the two above
   // single-step mode (vpm_plan_step): start state and control by value
   double u_const;
   int use_u_const;
@@ -445,7 +446,8 @@ __device__ __forceinline__ double control_at(const Args &a, int row, int t, cons
     u = a.u_const;
   } else if (a.pol_gains) {
     // evaluate_policy (policy.py:236-244): Python round() is round-half-even = rint
-    int k = (int)rint((tacc - a.pol_t_start) * a.P.inv_dt);
+    const double t_start = a.pol_times ? a.pol_times[0] : a.pol_t_start;
+    int k = (int)rint((tacc - t_start) * a.P.inv_dt);
     k = k < 0 ? 0 : (k > a.pol_h - 1 ? a.pol_h - 1 : k);
     double dot = 0.0;
     for (int j = 0; j < 7; ++j) dot += a.pol_gains[k * 7 + j] * (x[j] - a.pol_states[k * 7 + j]);
@@ -522,7 +524,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
       ctl->ring_b = a.snap_scal ? a.snap_scal[2] : a.ring_b;
       ctl->n_prev = sn_prev;
       ctl->lev_prev = a.snap_plev ? a.snap_plev[0] : a.prev_lev;
-      ctl->tacc = a.pol_t0;
+      ctl->tacc = a.pol_times ? a.pol_times[1] : a.pol_t0;
       ctl->lev_cur = 0.0;
       ctl->pending = 0;
       ctl->mcnt = min(MC, max(0, sn_wake + 3 - P.cap));
@@ -1276,8 +1278,15 @@ __global__ void mppi_combine_kernel(const double *__restrict__ parts, int W, int
 // x 2^32 + 4 per pair (iterations never overlap, whatever T), Box-Muller in FP64
 // (curand_normal2_double).  The value at (g, t) depends only on (seed, iteration,
 // g, t), so every sharding of the rows draws the same numbers; writes coalesce.
+// seed_iter (optional, graph replay): {seed, iteration} read on the device, the
+// iteration argument then being an offset added to it.
 __global__ void noise_philox_kernel(unsigned long long seed, unsigned long long iteration,
-                                    int row_begin, int rows, int T, double *__restrict__ out) {
+                                    int row_begin, int rows, int T, double *__restrict__ out,
+                                    const unsigned long long *__restrict__ seed_iter = nullptr) {
+  if (seed_iter) {
+    seed = seed_iter[0];
+    iteration += seed_iter[1];
+  }
   const int P = (T + 1) >> 1;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)rows * P) return;

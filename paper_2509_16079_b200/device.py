@@ -101,6 +101,16 @@ class DevicePlan:
         f, keep = fluid_struct(*flat)
         check(_lib.lib().vpm_plan_set_fluid(self.handle, C.byref(f)), "set_fluid")
 
+    def stage_fluid(self, fluid) -> None:
+        """Pack a snapshot into the pinned mirror without copying it up."""
+        flat = fluid.flat() if hasattr(fluid, "flat") else tuple(fluid)
+        f, keep = fluid_struct(*flat)
+        check(_lib.lib().vpm_plan_stage_fluid(self.handle, C.byref(f)), "stage_fluid")
+
+    def upload_fluid(self, stream=None) -> None:
+        """Queue the pinned mirror's copy to the device snapshot (graph-capturable)."""
+        check(_lib.lib().vpm_plan_upload_fluid(self.handle, _stream(stream, self.device)), "upload_fluid")
+
     # ---- rollouts -------------------------------------------------------------------
     def batch(self, x0, T: int, *, controls=None, ustar=None, noise=None, sigma: float = 0.0,
               row_begin: int = 0, rows: int | None = None, q=None, x_perch=None,
@@ -171,6 +181,17 @@ class DevicePlan:
             _stream(stream, self.device)), "plan_project")
         return status, final
 
+    def project_dev(self, x0, T: int, gains, states, inputs, times, stream=None):
+        """:meth:`project` with (t_start, t0) read from the device tensor ``times`` (2)
+        when the kernel runs (CUDA-graph replay); writes the plan's snapshot."""
+        torch = _torch()
+        status = torch.zeros(1, dtype=torch.int64, device=x0.device)
+        final = torch.empty(1, 7, dtype=torch.float64, device=x0.device)
+        check(_lib.lib().vpm_plan_project_dev(
+            self.handle, _p(x0), int(T), _p(gains), _p(states), _p(inputs), int(gains.shape[0]), _p(times),
+            _p(status), _p(final), 1, _stream(stream, self.device)), "plan_project_dev")
+        return status, final
+
     def cloud(self, x0, x0_noise, x0_scale, ustar, u_noise, sigma_u: float, stream=None):
         """Perturbed rollout cloud (policy.py:66-91): (status (K,), trajs (K, T+1, 7))."""
         torch = _torch()
@@ -218,6 +239,17 @@ def noise_philox(seed: int, iteration: int, out, row_begin: int = 0, stream=None
     with _on(out):
         check(_lib.lib().vpm_noise_philox(int(seed) & (2**64 - 1), int(iteration), int(row_begin), rows, T,
                                           _p(out), _stream(stream, out.device)), "noise_philox")
+    return out
+
+
+def noise_philox_dev(seed_iter, offset: int, out, row_begin: int = 0, stream=None):
+    """:func:`noise_philox` with {seed, iteration} read from the device int64 tensor
+    ``seed_iter`` (2) when the kernel runs (iteration + offset is drawn)."""
+    _need_f64(out, "out", 2)
+    rows, T = int(out.shape[0]), int(out.shape[1])
+    with _on(out):
+        check(_lib.lib().vpm_noise_philox_dev(_p(seed_iter), int(offset), int(row_begin), rows, T, _p(out),
+                                              _stream(stream, out.device)), "noise_philox_dev")
     return out
 
 

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import mppi
 from .config import ExperimentConfig
-from .device import noise_philox, policy_fit
+from .device import noise_philox, noise_philox_dev, policy_fit
 from .policy import NominalTrajectory, Policy, RankDeficientData, build_policy
 from .rollout import Engine
 from .vpm import FluidState
@@ -69,7 +69,7 @@ def _project_locked(plan, f64, policy, x, fluid, t, t_proj, engine):
 
 
 def replan(req: ReplanRequest, cfg: ExperimentConfig, engine: Engine,
-           rng: np.random.Generator) -> Policy | None:
+           rng: np.random.Generator, graph: bool = True) -> Policy | None:
     """Project, re-optimise, rebuild the policy (nmpc.py:106-134); None when rejected.
 
     The whole cycle is queued on one stream with a single host synchronisation at
@@ -85,11 +85,140 @@ def replan(req: ReplanRequest, cfg: ExperimentConfig, engine: Engine,
     caller's generator ends in the reference's state either way.
     With ``rng = mppi.DeviceNoise(seed)`` (performance mode) every draw -- the MPPI
     noise and the cloud's dx0 / du -- is made on the device instead and no host
-    random numbers are generated.
+    random numbers are generated; the whole cycle is then captured once per shape
+    as a CUDA graph and replayed (``graph=False``: queued launch by launch; both
+    give the same bits).
     """
     torch, plan, dev, _ = _dev(engine)
     with plan.lock:
+        if graph and isinstance(rng, mppi.DeviceNoise):
+            return _replan_graphed(torch, plan, dev, req, cfg, engine, rng)
         return _replan_locked(torch, plan, dev, req, cfg, engine, rng)
+
+
+class _ReplanGraph:
+    """A device-noise replan cycle captured as one CUDA graph for a fixed shape
+    (old-policy length, tail length H, K, iterations, cloud size, projection steps):
+    projection (times read on the device) -> iterations x (Philox noise with
+    seed / iteration read on the device + rollouts + partial + combine) -> nominal +
+    cloud -> clamp -> regression + Riccati -> the decision flags, nominal, u* and
+    gains copied to pinned host buffers.  Every per-call input -- the fluid snapshot
+    (the plan's pinned mirror), the small inputs and the Philox seed / iteration --
+    is copied up inside the graph from pinned memory at fixed addresses, so a
+    replay needs no argument updates."""
+
+    def __init__(self, torch, plan, dev, cfg, engine, hold: int, H: int, t_proj: int):
+        self.torch, self.plan, self.dev = torch, plan, dev
+        mc, sc = cfg.mppi, cfg.synthesis
+        self.K, self.iters, self.k, self.H, self.hold, self.t_proj = (int(mc.batch), int(mc.iterations),
+                                                                      int(sc.n_samples), H, hold, t_proj)
+        self.sizes = [H, 7, hold * 7, (hold + 1) * 7, hold, 7, 7, 7, 7, 7, 2]
+        self.offs = np.cumsum([0] + self.sizes)
+        f64, i64 = torch.float64, torch.int64
+        n_ints = 1 + max(self.iters, 1) + self.k + 1 + 1
+        self.h_head = torch.zeros(int(self.offs[-1]), dtype=f64, pin_memory=True)
+        self.h_si = torch.zeros(2, dtype=i64, pin_memory=True)
+        self.h_ints = torch.zeros(n_ints, dtype=i64, pin_memory=True)
+        self.h_traj = torch.zeros((H + 1) * 7, dtype=f64, pin_memory=True)
+        self.h_u = torch.zeros(H, dtype=f64, pin_memory=True)
+        self.h_gain = torch.zeros(H * 7, dtype=f64, pin_memory=True)
+        self.d_head = torch.zeros(int(self.offs[-1]), dtype=f64, device=dev)
+        self.d_si = torch.zeros(2, dtype=i64, device=dev)
+        self.consts = (float(mc.input_stdev), float(mc.temperature), float(sc.input_stdev), float(sc.r_running),
+                       float(engine.cfg.dt), float(engine.params.u_limit))
+        stream = torch.cuda.Stream(dev)
+        stream.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(stream):  # eager warm-up: scratch growth, kernel attributes
+            self._body()
+        stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=stream, capture_error_mode="thread_local"):
+            self._body()
+        stream.synchronize()
+
+    def _body(self):
+        torch, plan = self.torch, self.plan
+        H, K, iters, k, hold = self.H, self.K, self.iters, self.k, self.hold
+        sig, lam, sig_u, r_run, dt, lim = self.consts
+        plan.upload_fluid()  # the snapshot staged in the plan's pinned mirror
+        self.d_head.copy_(self.h_head, non_blocking=True)
+        self.d_si.copy_(self.h_si, non_blocking=True)
+        seg = [self.d_head[self.offs[i]:self.offs[i + 1]] for i in range(len(self.sizes))]
+        u, d_x = seg[0], seg[1]
+        d_gains, d_states, d_inputs = seg[2].view(hold, 7), seg[3].view(hold + 1, 7), seg[4]
+        q, xp, d_sx, d_qr, d_qf, d_times = seg[5], seg[6], seg[7], seg[8], seg[9], seg[10]
+        pstat, xdev = plan.project_dev(d_x, self.t_proj, d_gains, d_states, d_inputs, d_times)
+        x0 = xdev[0]
+        flags = torch.zeros(max(iters, 1), dtype=torch.int32, device=self.dev)
+        if H and iters and K:
+            scratch = {"cost": torch.empty(K + 1, dtype=torch.float64, device=self.dev),
+                       "partial": torch.empty(H + 2, dtype=torch.float64, device=self.dev)}
+            d_buf = torch.empty((K, H), dtype=torch.float64, device=self.dev)
+            for i in range(iters):
+                noise_philox_dev(self.d_si, i, d_buf)
+                scratch["flag"] = flags[i:i + 1]
+                plan.mppi_iteration(x0, u, d_buf, sig, K + 1, lam, q, xp, scratch)
+        dcl = torch.zeros((k + 1) * 7 + (k + 1) * H, dtype=torch.float64, device=self.dev)
+        d_cx = dcl[:(k + 1) * 7].view(k + 1, 7)
+        d_cu = dcl[(k + 1) * 7:].view(k + 1, H)
+        if k > 0:
+            noise_philox_dev(self.d_si, iters, d_cx[1:])
+            noise_philox_dev(self.d_si, iters + 1, d_cu[1:])
+        cstat, ctraj = plan.cloud(x0, d_cx, d_sx, u, d_cu, sig_u)
+        traj = ctraj[0]
+        cu_dev = torch.clamp(u.view(1, H) + d_cu[1:] * sig_u, -lim, lim)
+        _, _, _, _, d_gain, fflag = policy_fit(traj, u, ctraj[1:], cu_dev, cstat[1:], dt, d_qr, r_run, d_qf)
+        ints = torch.cat([pstat.view(1), flags.to(torch.int64), cstat, fflag[:1].to(torch.int64)])
+        self.h_ints.copy_(ints, non_blocking=True)
+        self.h_traj.copy_(traj.reshape(-1), non_blocking=True)
+        self.h_u.copy_(u, non_blocking=True)
+        self.h_gain.copy_(d_gain.reshape(-1), non_blocking=True)
+
+    def run(self, parts, seed: int, iteration: int):
+        hv = self.h_head.numpy()
+        for a, o in zip(parts, self.offs[:-1]):
+            hv[o:o + a.size] = a.ravel()
+        self.h_si.numpy()[:] = (np.int64(np.uint64(seed & (2**64 - 1)).view(np.int64)), iteration)
+        self.graph.replay()
+        self.torch.cuda.current_stream(self.dev).synchronize()
+        return (self.h_ints.numpy().copy(), self.h_traj.numpy().reshape(self.H + 1, 7).copy(),
+                self.h_u.numpy().copy(), self.h_gain.numpy().reshape(self.H, 7).copy())
+
+
+def _replan_graphed(torch, plan, dev, req, cfg, engine, rng):
+    dt = engine.cfg.dt
+    lim = engine.params.u_limit
+    old = req.policy.nominal
+    t_new = _projection_time(float(req.t), int(req.t_proj), dt)
+    k0 = int(round((t_new - old.t_start) / dt))
+    tail = old.inputs[k0:]
+    if len(tail) == 0:
+        return None
+    mc, sc = cfg.mppi, cfg.synthesis
+    H, iters, k = len(tail), int(mc.iterations), int(sc.n_samples)
+    gains = np.asarray(req.policy.gains, dtype=float)
+    hold = int(gains.shape[0])
+    key = (hold, H, int(req.t_proj), int(mc.batch), iters, k, float(mc.input_stdev), float(mc.temperature),
+           float(sc.input_stdev), float(sc.r_running), float(dt), float(lim))
+    cache = plan.__dict__.setdefault("_replan_graphs", {})
+    parts = [np.clip(np.asarray(tail, dtype=float), -lim, lim), np.asarray(req.x, dtype=float), gains,
+             np.asarray(old.states, dtype=float), np.asarray(old.inputs, dtype=float),
+             np.asarray(mc.q_terminal, dtype=float), np.asarray(mc.x_perch, dtype=float),
+             np.asarray(sc.state_stdev, dtype=float), np.asarray(sc.q_running, dtype=float),
+             np.asarray(sc.q_final, dtype=float), np.array([old.t_start, float(req.t)])]
+    plan.stage_fluid(req.fluid)
+    if key not in cache:
+        cache[key] = _ReplanGraph(torch, plan, dev, cfg, engine, hold, H, int(req.t_proj))
+    g = cache[key]
+    ints, traj, u, gain = g.run(parts, rng.seed, rng.iteration)
+    rng.iteration += iters + 2
+    st = ints[1 + max(iters, 1):1 + max(iters, 1) + k + 1]
+    if ints[0] != 0 or (H and iters and mc.batch and np.any(ints[1:1 + iters] != 0)) or st[0] != 0:
+        return None
+    if int((st[1:] == 0).sum()) < 6 or ints[-1] != 0:
+        return None
+    nominal = NominalTrajectory(states=traj, inputs=u, dt=dt, t_start=t_new)
+    return Policy(gains=gain, nominal=nominal, q_final=np.asarray(sc.q_final, dtype=float))
 
 
 def _replan_locked(torch, plan, dev, req, cfg, engine, rng):

@@ -132,6 +132,46 @@ def test_replan_with_device_noise(torch_cuda):
     assert w is None or not np.array_equal(w.gains, a.gains)
 
 
+def test_replan_graph_replay_equals_eager(torch_cuda):
+    """The device-noise replan captured as a CUDA graph and replayed gives bitwise
+    the launch-by-launch cycle, for several seeds through one cached graph, and a
+    second shape gets its own graph."""
+    import os
+    import time
+
+    from conftest import GOLDEN
+    from paper_2509_16079_b200 import config, mppi, replan as rp, rollout, vpm
+    from paper_2509_16079_b200.policy import NominalTrajectory, Policy
+    with np.load(os.path.join(GOLDEN, "nmpc_replan.npz")) as z:
+        gr = {k: z[k] for k in z.files}
+    cfg = config.ExperimentConfig()
+    eng = rollout.Engine.from_config(cfg)
+    pol = Policy(gains=gr["boot_gains"], nominal=NominalTrajectory(gr["boot_states"], gr["boot_inputs"], 0.01))
+    x0 = np.asarray(cfg.scenario.x0, float)
+    for t in (0.0, 0.1):
+        req = rp.ReplanRequest(x=x0, fluid=vpm.FluidState.empty(cfg.vpm), policy=pol, t=t, t_proj=10)
+        for seed in (3, 4, 5):
+            a = rp.replan(req, cfg, eng, mppi.DeviceNoise(seed), graph=True)
+            b = rp.replan(req, cfg, eng, mppi.DeviceNoise(seed), graph=False)
+            assert (a is None) == (b is None)
+            if a is not None:
+                np.testing.assert_array_equal(a.gains, b.gains)
+                np.testing.assert_array_equal(a.nominal.inputs, b.nominal.inputs)
+                np.testing.assert_array_equal(a.nominal.states, b.nominal.states)
+                assert a.nominal.t_start == b.nominal.t_start
+    plan = mppi.engine_plan(eng)
+    assert len(plan._replan_graphs) == 2
+    req = rp.ReplanRequest(x=x0, fluid=vpm.FluidState.empty(cfg.vpm), policy=pol, t=0.0, t_proj=10)
+    ms = {}
+    for g in (True, False):
+        rp.replan(req, cfg, eng, mppi.DeviceNoise(1), graph=g)
+        t0 = time.perf_counter()
+        for i in range(5):
+            rp.replan(req, cfg, eng, mppi.DeviceNoise(i), graph=g)
+        ms[g] = 1e3 * (time.perf_counter() - t0) / 5
+    print(f"replan e2e: graph {ms[True]:.3f} ms, eager {ms[False]:.3f} ms")
+
+
 def test_bootstrap_with_device_noise(torch_cuda):
     """bootstrap_policy (annealed MPPI + nominal + build_policy) runs end to end with
     a DeviceNoise generator and is deterministic."""
