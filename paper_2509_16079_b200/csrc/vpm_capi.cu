@@ -156,6 +156,7 @@ int build_inverses(const Phys &P, std::vector<double> &out) {
 
 struct Shape {
   int nt, r, w0, minb;  // threads, slots per sweeping warp, control-warp slots, reg variant
+  int sym = 0;          // symmetric-pair sweep (nt = 32 x tiles of 128 particles)
 };
 
 int device_sms() {
@@ -180,6 +181,40 @@ int device_sms() {
 // orders, see vpm_rollout.cuh).  VPM_SHAPE="nt,r" / VPM_MAXREG override for tuning.
 Shape pick_shape(int cap, int nb, int rows) {
   const int need = cap + 4;
+  const double per_sm = rows > 0 ? (double)rows / device_sms() : 1.0;
+  // Symmetric-pair sweep for caps above 256: T = ceil(cap / 128) warps of 128-particle
+  // tiles (vpm_rollout.cuh, sym_sweep).  The shape is a function of the cap alone, so
+  // every launch (single step, batch, any shard) of a given cap sums in the same
+  // order.  R >= 4 slots per thread (the tile) and >= cap + 4 targets for the direct
+  // fallback of overfull wakes.  VPM_SYM=0 selects the direct sweep (tuning / A-B).
+  const char *se = getenv("VPM_SYM");
+  if (cap > 256 && cap <= 2048 && !(se && atoi(se) == 0)) {
+    const int T = (cap + 127) / 128;
+    Shape s{32 * T, std::max(4, (need + 32 * T - 1) / (32 * T)), 0, 64, 1};
+    if (per_sm > 8.0) {
+      const int n_sm = (int)ceil(per_sm);
+      const size_t smem = vpm::make_layout(cap, nb, s.nt, true).total + 1024;
+      // register variants that leave fewer than 24 resident warps per SM are
+      // excluded (N = 2048, 512 threads: one CTA per SM at 72 registers)
+      auto slots = [&](int regs) {
+        int c = 65536 / (s.nt * regs);
+        c = std::min(c, 2048 / s.nt);
+        c = std::min(c, 32);
+        c = std::min(c, (int)((228 * 1024) / smem));
+        return (c < 1 || (regs > 64 && c * s.nt < 768)) ? 1 << 30 : ((n_sm + c - 1) / c) * c;
+      };
+      int bs = slots(64);
+      for (int regs : {72, 80}) {
+        const int sl = slots(regs);
+        if (sl <= bs) {
+          bs = sl;
+          s.minb = regs;
+        }
+      }
+    }
+    if (const char *m = getenv("VPM_MAXREG")) s.minb = atoi(m);
+    return s;
+  }
   if (const char *e = getenv("VPM_SHAPE")) {
     Shape s{0, 0, 0, 64};
     if (sscanf(e, "%d,%d", &s.nt, &s.r) == 2 && s.nt >= 64 && s.nt <= vpm::NT_MAX &&
@@ -188,7 +223,6 @@ Shape pick_shape(int cap, int nb, int rows) {
       return s;
     }
   }
-  const double per_sm = rows > 0 ? (double)rows / device_sms() : 1.0;
   Shape best{512, 8, 0, 64};
   if (per_sm <= 8.0) {
     // latency-bound launch (one round): the per-rollout critical path matters, so
@@ -277,10 +311,12 @@ cudaError_t launch_r(const Args &a, int grid, const Shape &sh, size_t smem, cuda
 
 cudaError_t launch_rollouts(Args a, int grid, cudaStream_t st) {
   const Shape sh = pick_shape(a.P.cap, a.P.nb, grid);
-  const size_t smem = vpm::make_layout(a.P.cap, a.P.nb, sh.nt).total;
+  a.sym = sh.sym;
+  const size_t smem = vpm::make_layout(a.P.cap, a.P.nb, sh.nt, sh.sym != 0).total;
 #ifdef VPM_TUNING_SUBSET
   // tuning builds (tools/): only the shapes the C4 / 8-GPU-shard / C2 launches pick
   if (sh.r == 5 && sh.minb == 72) return launch_t<5, 72>(a, grid, sh.nt, smem, st);
+  if (sh.r == 5 && sh.minb == 64) return launch_t<5, 64>(a, grid, sh.nt, smem, st);
   if (sh.r == 3 && sh.minb == 64) return launch_t<3, 64>(a, grid, sh.nt, smem, st);
   if (sh.r == 1 && sh.minb == 64) return launch_t<1, 64>(a, grid, sh.nt, smem, st);
   return cudaErrorNotSupported;
@@ -393,7 +429,7 @@ int vpm_launch_shape(int cap, int nb, int rows, int *threads, int *targets, int 
   const Shape s = pick_shape(cap, nb, rows);
   if (threads) *threads = s.nt;
   if (targets) *targets = s.r;
-  if (smem_bytes) *smem_bytes = vpm::make_layout(cap, nb, s.nt).total;
+  if (smem_bytes) *smem_bytes = vpm::make_layout(cap, nb, s.nt, s.sym != 0).total;
   return VPM_OK;
 }
 

@@ -163,6 +163,7 @@ struct Args {
   int use_x0v;
   int T, row_begin, rows;
   int integrate, check_envelope, need_fluid, record;
+  int sym;  // symmetric-pair convection sweep: NT = 32 T warps of 128-particle tiles
   // outputs (any may be null)
   int64_t *status;
   double *finals, *trajs, *cost;
@@ -196,7 +197,7 @@ struct Ctl {
   int holes[HOLES_MAX];
   int mcnt;     // merge candidates each warp keeps this step
   int fail, status, rc;
-  int cur;      // which of the two wake buffers holds the current (raw) wake
+  int cur;      // wake buffer of the output dump: 0, or 1 after a failure in D
   double tacc;  // feedback mode: simulation time, accumulated like nmpc.py:102
   // precomputed by warp 1 while warp 0 runs E of the previous step: the elevator
   // force of the pending step {Ex, Ez, xe_x, xe_z} and sincos(theta_t)
@@ -215,9 +216,11 @@ struct Layout {
 
 __host__ __device__ inline int align16(int v) { return (v + 15) & ~15; }
 
-__host__ __device__ inline Layout make_layout(int cap, int nb, int nt) {
+__host__ __device__ inline Layout make_layout(int cap, int nb, int nt, bool sym = false) {
   Layout L;
   L.capbuf = cap + WAKE_PAD;
+  // the symmetric sweep keeps its 2 x 128 T float2 reaction buffers in wake buffer 0
+  if (sym && L.capbuf < 4 * nt) L.capbuf = 4 * nt;
   L.nb = nb;
   L.S = nb + 2;
   L.RS = 2 * nb;                      // floats per source segment in the split sweeps
@@ -357,6 +360,235 @@ __device__ __noinline__ void sweep_dispatch(int kw, const float4 *src, int n, co
   }
 }
 
+// ---- symmetric-pair convection sweep (tile schedule) --------------------------------
+// Each unordered particle pair is evaluated once for both directions (the CPU core
+// does the same, _core.pyx:203-214): 11 FP32 lane-ops + 1 MUFU.RSQ per pair instead of
+// 2 x (8 + 1) for the two directed interactions.  The CTA has T warps; warp w owns the
+// tile of particles 128 w + 32 k + lane (slot k = 0..3, held as the packed slot pairs
+// (0,1) and (2,3)).  Pairs are covered as
+//   - the two diagonal super-blocks (slots 0,1 x particles of slots 0,1; 2,3 x 2,3):
+//     direct, sources as shared-memory broadcasts;
+//   - slots (0,1) x slots 2 and 3 of the same tile: lane rotation (below), the
+//     reaction comes home to the owning lane;
+//   - tile pairs (w, w+d), d = 1..(T-1)/2: warp w rotates every 32-particle block of
+//     tile w+d through its lanes; the reactions go to a shared-memory buffer that the
+//     owning warp adds after a barrier; for even T the pair (w, w+T/2) is split by
+//     target rows (warp w: its slots 0,1 x all of tile w+T/2; warp w+T/2: all its
+//     slots x blocks 2,3 of tile w).
+// Lane rotation: lane l loads source 32 J + l of a block as its "packet" and the packet
+// (coordinates and the reaction accumulated on it) moves one lane per step; after 32
+// steps each target met every source of the block and the packet is home.  No
+// cross-lane reduction and no atomics: every sum runs in a fixed order that depends
+// only on T and the particle indices, so a rollout's result is the same in every launch
+// with the same tile count (the launcher fixes T by the particle cap).
+
+// targets NP packed slot pairs vs sources [j0, j1) (broadcast)
+template <int NP>
+__device__ __forceinline__ void sym_direct(const float4 *__restrict__ src, int j0, int j1, const float2 *px,
+                                           const float2 *pz, float2 *qx, float2 *qz, float2 rc) {
+#pragma unroll 4
+  for (int j = j0; j < j1; ++j) {
+    const float4 s = src[j];
+    const float2 sx = make_float2(s.x, s.x), sz = make_float2(s.y, s.y), sg = make_float2(s.z, s.z);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const float2 dx = __fadd2_rn(sx, px[p]);
+      const float2 dz = __fadd2_rn(sz, pz[p]);
+      const float2 r2 = __ffma2_rn(dx, dx, __fmul2_rn(dz, dz));
+      const float2 q = __ffma2_rn(r2, r2, rc);
+      const float2 rs = make_float2(rsqrt_mufu(q.x), rsqrt_mufu(q.y));
+      const float2 c = __fmul2_rn(sg, rs);
+      qx[p] = __ffma2_rn(c, dz, qx[p]);
+      qz[p] = __ffma2_rn(c, dx, qz[p]);
+    }
+  }
+}
+
+// the two diagonal super-blocks at once: pair 0 vs sources [b0, b0 + n0), pair 1 vs
+// [b1, b1 + n1), n1 <= n0 (two independent chains per iteration)
+__device__ __forceinline__ void sym_direct_diag(const float4 *__restrict__ src, int b0, int n0, int b1, int n1,
+                                                const float2 *px, const float2 *pz, float2 *qx, float2 *qz,
+                                                float2 rc) {
+#pragma unroll 4
+  for (int j = 0; j < n1; ++j) {
+    const float4 s0 = src[b0 + j], s1 = src[b1 + j];
+    const float2 sx[2] = {make_float2(s0.x, s0.x), make_float2(s1.x, s1.x)};
+    const float2 sz[2] = {make_float2(s0.y, s0.y), make_float2(s1.y, s1.y)};
+    const float2 sg[2] = {make_float2(s0.z, s0.z), make_float2(s1.z, s1.z)};
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const float2 dx = __fadd2_rn(sx[p], px[p]);
+      const float2 dz = __fadd2_rn(sz[p], pz[p]);
+      const float2 r2 = __ffma2_rn(dx, dx, __fmul2_rn(dz, dz));
+      const float2 q = __ffma2_rn(r2, r2, rc);
+      const float2 rs = make_float2(rsqrt_mufu(q.x), rsqrt_mufu(q.y));
+      const float2 c = __fmul2_rn(sg[p], rs);
+      qx[p] = __ffma2_rn(c, dz, qx[p]);
+      qz[p] = __ffma2_rn(c, dx, qz[p]);
+    }
+  }
+  sym_direct<1>(src, b0 + n1, b0 + n0, px, pz, qx, qz, rc);
+}
+
+// NK packets (sx, sz, sg) rotated together through the lanes against NP packed
+// target pairs (px, pz = negated target coordinates, pg = negated target Gamma/2pi);
+// per step every packet meets the targets in packet order.  Returns the reaction on
+// the lane's own packet sources in the (ax, az) convention.
+template <int NP, int NK>
+__device__ __forceinline__ void sym_rotate(float *sx, float *sz, float *sg, const float2 *px, const float2 *pz,
+                                           const float2 *pg, float2 *qx, float2 *qz, float2 rc, int nxt,
+                                           float *rbx, float *rbz) {
+  float2 bx[NK], bz[NK];
+#pragma unroll
+  for (int k = 0; k < NK; ++k) bx[k] = bz[k] = make_float2(0.f, 0.f);
+#pragma unroll(NK == 1 ? 4 : 2)
+  for (int r = 0; r < 32; ++r) {
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+      const float2 sx2 = make_float2(sx[k], sx[k]), sz2 = make_float2(sz[k], sz[k]),
+                   sg2 = make_float2(sg[k], sg[k]);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const float2 dx = __fadd2_rn(sx2, px[p]);
+        const float2 dz = __fadd2_rn(sz2, pz[p]);
+        const float2 r2 = __ffma2_rn(dx, dx, __fmul2_rn(dz, dz));
+        const float2 q = __ffma2_rn(r2, r2, rc);
+        const float2 rs = make_float2(rsqrt_mufu(q.x), rsqrt_mufu(q.y));
+        const float2 cj = __fmul2_rn(sg2, rs);
+        qx[p] = __ffma2_rn(cj, dz, qx[p]);
+        qz[p] = __ffma2_rn(cj, dx, qz[p]);
+        const float2 ci = __fmul2_rn(pg[p], rs);  // -g_target rs: reaction (t - s = -d')
+        bx[k] = __ffma2_rn(ci, dz, bx[k]);
+        bz[k] = __ffma2_rn(ci, dx, bz[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+      sx[k] = __shfl_sync(0xffffffffu, sx[k], nxt);
+      sz[k] = __shfl_sync(0xffffffffu, sz[k], nxt);
+      sg[k] = __shfl_sync(0xffffffffu, sg[k], nxt);
+      bx[k].x = __shfl_sync(0xffffffffu, bx[k].x, nxt);
+      bx[k].y = __shfl_sync(0xffffffffu, bx[k].y, nxt);
+      bz[k].x = __shfl_sync(0xffffffffu, bz[k].x, nxt);
+      bz[k].y = __shfl_sync(0xffffffffu, bz[k].y, nxt);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    rbx[k] = bx[k].x + bx[k].y;
+    rbz[k] = bz[k].x + bz[k].y;
+  }
+}
+
+__device__ __forceinline__ float &slot_ref(float2 *v, int k) { return (k & 1) ? v[k >> 1].y : v[k >> 1].x; }
+
+// The whole convection sweep of warp w (all warps call it: it contains the round
+// barriers).  wb = compacted wake (nl particles), rb = reaction buffers (2 x 128 T
+// float2, tile v's entries in float2 [256 v, 256 v + 256) so that the later advection
+// writes of warp v only overwrite entries warp v has already consumed), psrc = previous
+// bound row.  Returns (ax, az) of the warp's 4 slots; u_x = -ax, u_z = az.
+__device__ __noinline__ void sym_sweep(const float4 *__restrict__ wb, float2 *rb, int nl,
+                                       const float4 *__restrict__ psrc, int n_prev, float rc4, int T, int w,
+                                       float *ax4, float *az4) {
+  const int lane = threadIdx.x & 31, nxt = (lane + 1) & 31;
+  const float2 rc = make_float2(rc4, rc4);
+  const int base = 128 * w;
+  float2 px[2], pz[2], pg[2], qx[2], qz[2];
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int c0 = base + 64 * p + lane, c1 = c0 + 32;
+    const float4 v0 = c0 < nl ? wb[c0] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 v1 = c1 < nl ? wb[c1] : make_float4(0.f, 0.f, 0.f, 0.f);
+    px[p] = make_float2(-v0.x, -v1.x);
+    pz[p] = make_float2(-v0.y, -v1.y);
+    pg[p] = make_float2(-v0.z, -v1.z);
+    qx[p] = make_float2(0.f, 0.f);
+    qz[p] = make_float2(0.f, 0.f);
+  }
+  const bool act0 = base < nl, act1 = base + 64 < nl;
+  // previous bound row and the diagonal super-blocks, direct
+  if (act1) {
+    sym_direct<2>(psrc, 0, n_prev, px, pz, qx, qz, rc);
+    sym_direct_diag(wb, base, 64, base + 64, min(64, nl - base - 64), px, pz, qx, qz, rc);
+    // slots (0,1) x the particles of slots 2 and 3 (two packets together)
+    float sx[2] = {-px[1].x, -px[1].y}, sz[2] = {-pz[1].x, -pz[1].y}, sg[2] = {-pg[1].x, -pg[1].y};
+    float rbx[2], rbz[2];
+    sym_rotate<1, 2>(sx, sz, sg, px, pz, pg, qx, qz, rc, nxt, rbx, rbz);
+    qx[1].x += rbx[0];
+    qz[1].x += rbz[0];
+    qx[1].y += rbx[1];
+    qz[1].y += rbz[1];
+  } else if (act0) {
+    sym_direct<1>(psrc, 0, n_prev, px, pz, qx, qz, rc);
+    sym_direct<1>(wb, base, min(base + 64, nl), px, pz, qx, qz, rc);
+  }
+  // tile pairs (w, w+d): warp w rotates tile w+d's blocks, the owner adds the reactions.
+  // Blocks m0..m1-1 of tile v against np target pairs; pairs of blocks go together
+  // when only target pair 0 takes part (more independent chains per step).
+  auto sweep_blocks = [&](int v, int m0, int m1, int np, float2 *dst) {
+    int m = m0;
+    while (m < m1 && 128 * v + 32 * m < nl) {
+      const int j = 128 * v + 32 * m;
+      if (np == 1 && m + 1 < m1 && j + 32 < nl) {
+        const float4 s0 = j + lane < nl ? wb[j + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 s1 = j + 32 + lane < nl ? wb[j + 32 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float sx[2] = {s0.x, s1.x}, sz[2] = {s0.y, s1.y}, sg[2] = {s0.z, s1.z};
+        float rbx[2], rbz[2];
+        sym_rotate<1, 2>(sx, sz, sg, px, pz, pg, qx, qz, rc, nxt, rbx, rbz);
+        dst[32 * m + lane] = make_float2(rbx[0], rbz[0]);
+        dst[32 * m + 32 + lane] = make_float2(rbx[1], rbz[1]);
+        m += 2;
+      } else {
+        const float4 s0 = j + lane < nl ? wb[j + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float sx[1] = {s0.x}, sz[1] = {s0.y}, sg[1] = {s0.z};
+        float rbx[1], rbz[1];
+        if (np == 2) sym_rotate<2, 1>(sx, sz, sg, px, pz, pg, qx, qz, rc, nxt, rbx, rbz);
+        else sym_rotate<1, 1>(sx, sz, sg, px, pz, pg, qx, qz, rc, nxt, rbx, rbz);
+        dst[32 * m + lane] = make_float2(rbx[0], rbz[0]);
+        m += 1;
+      }
+    }
+  };
+  auto receive = [&](const float2 *src, int k0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < k0 || base + 32 * k >= nl) continue;
+      const float2 r = src[32 * k + lane];
+      slot_ref(qx, k) += r.x;
+      slot_ref(qz, k) += r.y;
+    }
+  };
+  const int np = act1 ? 2 : 1;
+  const int D = (T - 1) >> 1;
+  for (int d = 1; d <= D; ++d) {
+    const int v = w + d < T ? w + d : w + d - T;
+    if (act0) sweep_blocks(v, 0, 4, np, rb + 256 * v + 128 * (d & 1));
+    __syncthreads();
+    const int u = w - d >= 0 ? w - d : w - d + T;  // the warp that rotated this tile
+    if (act0 && 128 * u < nl) receive(rb + 256 * w + 128 * (d & 1), 0);
+  }
+  if (T >= 2 && (T & 1) == 0) {
+    const int d = T >> 1;
+    if (w < d) {  // slots 0,1 x all of tile w+d
+      if (act0) sweep_blocks(w + d, 0, 4, 1, rb + 256 * (w + d) + 128 * (d & 1));
+    } else {  // all slots x blocks 2,3 of tile w-d
+      if (act0) sweep_blocks(w - d, 2, 4, np, rb + 256 * (w - d) + 128 * (d & 1));
+    }
+    __syncthreads();
+    if (w < d) {
+      if (act1 && 128 * (w + d) < nl) receive(rb + 256 * w + 128 * (d & 1), 2);
+    } else {
+      if (act0 && 128 * (w - d) < nl) receive(rb + 256 * w + 128 * (d & 1), 0);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    ax4[k] = slot_ref(qx, k);
+    az4[k] = slot_ref(qz, k);
+  }
+}
+
 // Deterministic butterfly-transpose reduction of 8 floats across a warp:
 // afterwards every lane holds the full sum of value index (lane >> 2).
 __device__ __forceinline__ float warp_reduce8(float v[8], int lane) {
@@ -472,7 +704,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
   const Phys &P = a.P;
   const int nb = P.nb;
   const int NT = blockDim.x, NW = NT >> 5;
-  const Layout L = make_layout(P.cap, nb, NT);
+  const Layout L = make_layout(P.cap, nb, NT, a.sym != 0);
   float4 *wbuf = reinterpret_cast<float4 *>(smem);  // two wake buffers of capbuf
   float4 *psrc = reinterpret_cast<float4 *>(smem + L.off_psrc);
   float2 *st = reinterpret_cast<float2 *>(smem + L.off_st);
@@ -549,15 +781,21 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
     const bool pend = ctl->pending;
     const int n_raw = ctl->n_raw, n_live = ctl->n_live, nh = ctl->n_holes;
     const int n_prev = ctl->n_prev;
-    const int cur = ctl->cur;
-    const float4 *wsrc = wbuf + cur * L.capbuf;  // raw wake of this iteration (read-only)
-    float4 *wk = wbuf + (cur ^ 1) * L.capbuf;    // compacted, advected wake being built
+    // Buffer 0 holds the wake (raw: removed particles are zero-circulation holes until
+    // the next advection compacts them); buffer 1 receives a compacted copy at the top
+    // of every convecting iteration, which the convection sweep reads (sources and
+    // targets), while the advection writes the new wake back into buffer 0.
+    float4 *wake = wbuf;
+    float4 *wcmp = wbuf + L.capbuf;
+    const bool sym = a.sym && conv && n_live <= 128 * NW;  // uniform over the CTA
 
     // ---------------- P1: wake velocity at the panels of step t-1 (its loads),
     // source-split over all warps.  (Carrying the 10 panel targets in one warp's
     // register sweep instead costs that warp a whole extra 32-target slot -- +25%
     // on the critical path at N=512 -- so the split sweep stays.)
-    if (pend) split_sweep(wsrc, n_raw, st, nb, rc4, red, RS, tid, NT);
+    if (pend) split_sweep(wake, n_raw, st, nb, rc4, red, RS, tid, NT);
+    if (conv)
+      for (int c = tid; c < n_live; c += NT) wcmp[c] = wake[nh ? raw_index(c, ctl->holes, nh) : c];
     PHASE_MARK(0);
     __syncthreads();  // B1
     PHASE_MARK(1);
@@ -670,11 +908,15 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           for (int i = 0; i < 7; ++i)
             if (lane == i) ctl->x[i] = xn[i];
           if (lane == 0) {
+            bool failed = false;
             if (!fin) {
-              ctl->fail = 1; ctl->status = t; ctl->rc = 2;
+              ctl->fail = 1; ctl->status = t; ctl->rc = 2; failed = true;
             } else if (a.check_envelope && (fabs(xn[6]) > 300.0 || fabs(xn[4]) > 80.0 || fabs(xn[5]) > 80.0)) {
-              ctl->fail = 1; ctl->status = t; ctl->rc = 0;
+              ctl->fail = 1; ctl->status = t; ctl->rc = 0; failed = true;
             }
+            // the failure-time wake: this iteration's advection already rewrote
+            // buffer 0, its compacted copy in buffer 1 is the wake of step t-1
+            if (failed && conv) { ctl->cur = 1; ctl->n_raw = n_live; ctl->n_holes = 0; }
           }
         }
         __syncwarp();
@@ -733,21 +975,28 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
       PHASE_MARK(2);
     }
     const int wslot = SLOT_REV ? NW - 1 - warp : warp;
-    if (pass != D_PASS && conv && 32 * wslot >= n_live) {
+    if (pass != D_PASS && conv && !sym && 32 * wslot >= n_live) {
       // a warp without live targets (small wakes) only clears its merge candidates
       if (lane == 0)
         for (int r = 0; r < ctl->mcnt; ++r) cand[warp * MC + r] = 0u;
     } else if (pass != D_PASS && conv) {
-      // ---------------- P2, all warps: S1 convection sweep of step t, then A
-      // (reads the raw buffer, writes the other one: no read/write race with
-      //  the warps still sweeping, and on a failure in D the raw buffer still
-      //  holds the reference's failure-time wake).  Slot k of warp w holds the
-      //  particles c = 32 (NW k + NW-1-w) + lane (the odd block lands on the last
-      //  warp, not on warp 0, which runs D after its slots).
-      const int kmax = R;
-      auto slot_base = [&](int k) { return 32 * (NW * k + wslot); };
+      // ---------------- P2, all warps: S1 convection sweep of step t over the
+      // compacted copy, then A (advect into buffer 0).  Direct path: slot k of warp w
+      // holds the particles c = 32 (NW k + NW-1-w) + lane (the odd block lands on the
+      // last warp, not on warp 0, which runs D after its slots).  Symmetric path:
+      // warp w holds c = 128 w + 32 k + lane, k < 4.
+      const int kmax = sym ? (R < 4 ? R : 4) : R;
+      auto slot_base = [&](int k) { return sym ? 128 * warp + 32 * k : 32 * (NW * k + wslot); };
       float ux[R], uz[R];
-      {
+      if (sym) {
+        float ax4[4], az4[4];
+        sym_sweep(wcmp, reinterpret_cast<float2 *>(wake), n_live, psrc, n_prev, rc4, NW, warp, ax4, az4);
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          ux[k] = k < 4 ? -ax4[k < 4 ? k : 0] : 0.f;
+          uz[k] = k < 4 ? az4[k < 4 ? k : 0] : 0.f;
+        }
+      } else {
         float ntx[R], ntz[R], bx_[R], bz_[R];
         int kw = 0;
 #pragma unroll
@@ -755,19 +1004,19 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           const int c = slot_base(k) + lane;
           ntx[k] = 0.f;
           ntz[k] = 0.f;
-          if (k < kmax && c < n_live) {
-            const float4 v = wsrc[raw_index(c, ctl->holes, nh)];
+          if (c < n_live) {
+            const float4 v = wcmp[c];
             ntx[k] = -v.x;
             ntz[k] = -v.y;
           }
-          if (k < kmax && slot_base(k) < n_live) kw = k + 1;
+          if (slot_base(k) < n_live) kw = k + 1;
           ux[k] = 0.f;
           uz[k] = 0.f;
           bx_[k] = 0.f;
           bz_[k] = 0.f;
         }
         if (kw > 0) {  // a warp without live targets skips the calls (and their spills)
-          sweep_dispatch<R>(kw, wsrc, n_raw, ntx, ntz, ux, uz, rc4);
+          sweep_dispatch<R>(kw, wcmp, n_live, ntx, ntz, ux, uz, rc4);
           sweep_dispatch<R>(kw, psrc, n_prev, ntx, ntz, bx_, bz_, rc4);
         }
 #pragma unroll
@@ -776,7 +1025,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           uz[k] = uz[k] + bz_[k];
         }
       }
-      // A: advect / dissipate / age into the compacted slot c (_core.pyx:222-226)
+      // A: advect / dissipate / age into slot c of buffer 0 (_core.pyx:222-226)
       const int ra = ctl->ring_a, rb = ctl->ring_b;
       unsigned keys[R];
 #pragma unroll
@@ -785,12 +1034,12 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
         keys[k] = 0u;
         double g = 0.0;
         if (k < kmax && c < n_live) {
-          const float4 v = wsrc[raw_index(c, ctl->holes, nh)];
+          const float4 v = wcmp[c];
           const float nxp = (float)((double)v.x + dt * (double)ux[k]);
           const float nzp = (float)((double)v.y + dt * (double)uz[k]);
           const float ng = (float)((double)v.z * P.k_diss);
           const int na = __float_as_int(v.w) + 1;
-          wk[c] = make_float4(nxp, nzp, ng, __int_as_float(na));
+          wake[c] = make_float4(nxp, nzp, ng, __int_as_float(na));
           g = (double)ng;
           if (c != ra && c != rb) keys[k] = ((unsigned)(na + 1) << 12) | (unsigned)(4095 - c);
         }
@@ -823,7 +1072,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
     if (!conv || ctl->fail) break;
 
     // ---------------- S2: wake velocity at the collocation rows of step t
-    split_sweep(wk, n_live, st, nb, rc4, red, RS, tid, NT);
+    split_sweep(wake, n_live, st, nb, rc4, red, RS, tid, NT);
     PHASE_MARK(5);
     __syncthreads();  // B3
     PHASE_MARK(6);
@@ -899,14 +1148,14 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
       if (!ok) {
         if (lane == 0) {
           ctl->fail = 1; ctl->status = t + 1; ctl->rc = 2;
-          ctl->n_raw = nl; ctl->n_holes = 0; ctl->cur = cur ^ 1;
+          ctl->n_raw = nl; ctl->n_holes = 0;
         }
       } else {
         const double levg = shed ? gam[nb] : 0.0;
         int n_now = nl;
         if (shed) {
-          if (lane == 0) wk[nl] = make_float4((float)ctl->lx, (float)ctl->lz, (float)(gam[nb] * INV_TWO_PI), __int_as_float(0));
-          if (lane == 1) wk[nl + 1] = make_float4((float)ctl->tx, (float)ctl->tz, (float)(gam[nb + 1] * INV_TWO_PI), __int_as_float(0));
+          if (lane == 0) wake[nl] = make_float4((float)ctl->lx, (float)ctl->lz, (float)(gam[nb] * INV_TWO_PI), __int_as_float(0));
+          if (lane == 1) wake[nl + 1] = make_float4((float)ctl->tx, (float)ctl->tz, (float)(gam[nb + 1] * INV_TWO_PI), __int_as_float(0));
           n_now = nl + 2;
         }
         __syncwarp();
@@ -946,21 +1195,21 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           if (nsel >= 2) {
             const int merges = min(m, nsel - 1);
             const int idx0 = 4095 - (int)(sel[0] & 4095u);
-            float4 blob = wk[idx0];
+            float4 blob = wake[idx0];
             int lo = idx0;
             int ids[MC];
             ids[0] = idx0;
             for (int r = 1; r <= merges; ++r) {
               const int id = 4095 - (int)(sel[r] & 4095u);
               ids[r] = id;
-              const float4 p = wk[id];
+              const float4 p = wake[id];
               blob.x = 0.5f * (blob.x + p.x);
               blob.y = 0.5f * (blob.y + p.y);
               blob.z = blob.z + p.z;
               lo = min(lo, id);
             }
             __syncwarp();
-            if (lane == 0) wk[lo] = blob;
+            if (lane == 0) wake[lo] = blob;
             for (int r = 0; r <= merges; ++r)
               if (ids[r] != lo) hl[nholes++] = ids[r];
           }
@@ -968,7 +1217,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
         // ---- ring termination against the offset chord (_core.pyx:359-373)
         if (ra >= 0 && rb >= 0) {
           __syncwarp();
-          const float4 A0 = wk[ra], A1 = wk[rb];
+          const float4 A0 = wake[ra], A1 = wake[rb];
           const double fx = ctl->fx, fz = ctl->fz;
           const double ox = -0.02 * P.l_chord * nx, oz = -0.02 * P.l_chord * nz;
           const double ax0 = A0.x, az0 = A0.y, ax1 = A1.x, az1 = A1.y;
@@ -998,7 +1247,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           hl[j + 1] = v;
         }
         __syncwarp();
-        if (lane < nholes) wk[hl[lane]].z = 0.f;
+        if (lane < nholes) wake[hl[lane]].z = 0.f;
         int ra2 = ra, rb2 = rb;
         for (int h = 0; h < nholes; ++h) {
           if (ra >= 0 && hl[h] < ra) --ra2;
@@ -1023,7 +1272,6 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           ctl->ring_a = ra2;
           ctl->ring_b = rb2;
           ctl->mcnt = min(MC, max(0, n_live_next + 3 - P.cap));
-          ctl->cur = cur ^ 1;
           if (shed && t < 64) ctl->shed_mask |= 1ull << t;
           if (shed && t >= 64 && t < 128) ctl->shed_hi |= 1ull << (t - 64);
           ctl->whash = wake_sig_step(ctl->whash, n_live_next, ra2, rb2, shed);
