@@ -514,9 +514,16 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         if backend == "nccl":
+            # NCCL's communicator setup lines (nranks, NVLS / P2P transports) go to
+            # stderr, so a run's log shows that N ranks formed one communicator
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        if rank == 0:
+            ver = torch.cuda.nccl.version() if backend == "nccl" else None
+            print(f"bench: {world} ranks, backend {backend}, NCCL {ver}", file=sys.stderr, flush=True)
     from paper_2509_16079_b200 import _lib
     from paper_2509_16079_b200.device import DevicePlan, fp32_peak_gflops, launch_shape
     from paper_2509_16079_b200.sharding import ShardedMppi

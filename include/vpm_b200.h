@@ -71,8 +71,14 @@ typedef struct vpm_fluid_out {
 /* ---- layer 1: reference-facing, host buffers -------------------------------- */
 
 /* One coupled step (integrate=1: Engine.step, 0: Engine.fluid_step).  x is
- * in/out (7).  Returns the step rc (0 ok, 1 singular solve, 2 non-finite) or a
- * negative error.  fw (2) and mw (1) receive the wing loads.  _core.pyx:536-576 */
+ * in/out (7).  Returns the step rc (0 ok, 2 non-finite) or a negative error.  fw
+ * (2) and mw (1) receive the wing loads.  _core.pyx:536-576.
+ * The reference's rc 1 (zero LU pivot in the boundary solve, _core.pyx:315-317)
+ * cannot occur here: the three boundary systems are pose-invariant (they couple
+ * points on the chord line only), so they are factorised once when the parameters
+ * are unpacked and a singular one is reported as VPM_ERR_CONFIG ("boundary system is
+ * singular for this configuration") before any step runs -- the configuration for
+ * which the reference would return rc 1 at its first shedding or attached step. */
 int vpm_step(double *x, double u, const vpm_fluid *fluid, const int64_t *iparams,
              const double *fparams, int integrate, double *fw, double *mw, vpm_fluid_out *out);
 

@@ -18,16 +18,20 @@
 //
 //   P1  all warps, source-split: wake velocity at the panels of step t-1 (the
 //       loads of step t-1, _core.pyx:385-389; the sources are the post-merge wake,
-//       i.e. exactly the sources of the convection sweep of step t).
+//       i.e. exactly the sources of the convection sweep of step t); the live wake
+//       is copied, compacted, into buffer 1.
 //   B1
-//   P2  warp 0 first runs D: unsteady-Bernoulli loads of step t-1
+//   P2  the control warp (warp 0; the last warp with the symmetric sweep) runs D
+//       after its share of S1/A: unsteady-Bernoulli loads of step t-1
 //       (_core.pyx:375-418), elevator + Euler integration (_core.pyx:423-461),
 //       envelope check (_core.pyx:483-484), then the chord frame / collocation
 //       geometry, gates and control of step t (_core.pyx:228-256).
 //       All warps: S1 = velocity at every live wake particle from every wake
-//       particle + the previous bound row (convection, _core.pyx:192-221), register
-//       tiled; then A = Euler advection, dissipation, ageing (_core.pyx:222-226),
-//       read from the raw buffer and written compacted into the other buffer
+//       particle + the previous bound row (convection, _core.pyx:192-221) over the
+//       compacted copy of the wake made before B1 (buffer 1) -- register-tiled
+//       direct sums, or for caps above 256 the symmetric-pair tile schedule
+//       (sym_sweep, with one barrier per tile round); then A = Euler advection,
+//       dissipation, ageing (_core.pyx:222-226) written compacted into buffer 0
 //       (this retires the ordered removals of step t-1); Kelvin block sums;
 //       per-warp merge candidates.
 //   B2
