@@ -651,7 +651,7 @@ def test_optimize_pipeline_equals_host_entry_and_rewinds_on_failure(torch_cuda):
 @pytest.mark.parametrize("N", [1024, 2048])
 def test_c5_large_wake_vs_oracle(torch_cuda, oracle_core, N):
     """C5-scale wakes (N = 1024 / 2048, random wake, attached flow so N
-    stays fixed; launch shapes 512 x 3 / 512 x 5): a few rollouts of 5 steps
+    stays fixed; symmetric-pair sweep on 8 / 16 tiles): a few rollouts of 5 steps
     against the FP64 oracle on identical inputs -- final states, and the wake the
     single-rollout path returns."""
     from paper_2509_16079_b200 import config, rollout, vpm
@@ -674,3 +674,47 @@ def test_c5_large_wake_vs_oracle(torch_cuda, oracle_core, N):
     assert rc == rc_o == 0 and fl_g.n_wake == flat_o[3] == N
     np.testing.assert_array_equal(fl_g.wake_age[:N], flat_o[2][:N])
     assert_close(fl_g.wake_pos[:N], flat_o[0][:N], "wake_pos", what=f"C5 N={N} wake")
+
+
+@pytest.mark.parametrize("cap,n0", [(400, 300), (300, 290), (640, 600), (512, 516), (1000, 900)])
+def test_symmetric_tiles_vs_oracle(torch_cuda, oracle_core, cap, n0):
+    """The symmetric-pair tile schedule at the edges of its tiling: partial and empty
+    tiles (cap 400 / wake 300), odd tile counts (cap 300: 3 tiles, cap 640: 5),
+    eight tiles with a partial last one (cap 1000), and an overfull snapshot
+    (cap + 4 particles: the first step takes the direct fallback); shedding plate,
+    wakes growing into the cap and merging.  Decisions (status, shed steps, final wake
+    size, wake-index signature) exact off near-ties, trajectories within the stated
+    tolerance, and every single-rollout call bitwise equal to its row of the batch
+    (the tile count depends on the cap only)."""
+    torch = torch_cuda
+    from paper_2509_16079_b200 import config, rollout, vpm
+    from paper_2509_16079_b200.device import DevicePlan
+    rng = np.random.default_rng(cap + n0)
+    v = config.VpmConfig(particle_cap=cap)
+    eng = rollout.Engine(v, config.GliderParams())
+    fl = vpm.FluidState.empty(v)
+    fl.wake_pos[:n0] = rng.normal(0.0, 0.5, (n0, 2)) - np.array([3.0, 0.0])
+    fl.wake_gamma[:n0] = rng.normal(0.0, 0.02, n0)
+    fl.wake_age[:n0] = rng.integers(0, 400, n0)
+    fl.n_wake = n0
+    B, T = 6, 30
+    ctrl = np.clip(-6.0 + 3.0 * rng.normal(0.0, 1.0, (B, T)), -15, 15)
+    plan = DevicePlan(eng.iparams, eng.fparams)
+    plan.set_fluid(fl.flat())
+    dev = torch.device("cuda")
+    out = plan.batch(torch.as_tensor(X0, device=dev), T, controls=torch.as_tensor(ctrl, device=dev), rows=B,
+                     diagnostics=True)
+    torch.cuda.synchronize()
+    gpu = {k: t.cpu().numpy() for k, t in out.items()}
+    d = oracle_core.batch_rollout_diag(X0, ctrl, *fl.flat(), eng.iparams, eng.fparams, record=True)
+    ok = _check_decisions(gpu, d, f"cap {cap}, wake {n0}")
+    assert ok.sum() >= 3
+    res = eng.batch(rollout.RolloutRequest(x0=X0, fluid=fl, controls=ctrl, record=True))
+    np.testing.assert_array_equal(res.status, gpu["status"])
+    np.testing.assert_array_equal(res.trajectories[:, -1][res.status == 0], gpu["finals"][res.status == 0])
+    assert_close(res.trajectories[ok], d["trajs"][ok], what=f"cap {cap} wake {n0} trajs")
+    for k in range(B):
+        rc, traj, _ = eng.rollout(X0, ctrl[k], fl, record=True)
+        assert rc == res.status[k]
+        if rc == 0:
+            np.testing.assert_array_equal(traj, res.trajectories[k])

@@ -251,6 +251,69 @@ __global__ void __maxnreg__(MAXREG) rotl_kernel(float *out, int n, int reps, flo
   if (s == 1.2345f) out[blockIdx.x] = s;
 }
 
+// Source-packed rotation: each lane's packet holds two sources (float2), the four
+// targets are scalar broadcasts: 10 shuffles per 8 pairs instead of 7 per 4.
+template <int MAXREG, int UNR>
+__global__ void __maxnreg__(MAXREG) rotsp_kernel(float *out, int n, int reps, float rc4) {
+  extern __shared__ float4 src[];
+  fill(src, n);
+  float *part = reinterpret_cast<float *>(src + n);
+  const int lane = threadIdx.x & 31;
+  float tx[4], tz[4], tg[4];
+  float2 ax[4], az[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    tx[i] = -0.013f * (threadIdx.x + i);
+    tz[i] = -0.011f * i - 0.019f * (threadIdx.x & 3);
+    tg[i] = 1e-3f * (i + 1) * ((lane & 1) ? -1.f : 1.f);
+    ax[i] = az[i] = make_float2(0.f, 0.f);
+  }
+  const float2 rc = make_float2(rc4, rc4);
+  const int nxt = (lane + 1) & 31;
+  for (int rep = 0; rep < reps; ++rep) {
+    for (int J0 = 0; J0 < n / 32; J0 += 2) {
+      const float4 s0 = src[32 * J0 + lane], s1 = src[32 * J0 + 32 + lane];
+      float2 sx = make_float2(s0.x, s1.x), sz = make_float2(s0.y, s1.y), sg = make_float2(s0.z, s1.z);
+      float2 bx = make_float2(0.f, 0.f), bz = make_float2(0.f, 0.f);
+#pragma unroll UNR
+      for (int r = 0; r < 32; ++r) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 dx = __fadd2_rn(sx, make_float2(tx[i], tx[i]));
+          const float2 dz = __fadd2_rn(sz, make_float2(tz[i], tz[i]));
+          const float2 r2 = __ffma2_rn(dx, dx, __fmul2_rn(dz, dz));
+          const float2 q = __ffma2_rn(r2, r2, rc);
+          const float2 rs = make_float2(rsq(q.x), rsq(q.y));
+          const float2 cj = __fmul2_rn(sg, rs);
+          ax[i] = __ffma2_rn(cj, dz, ax[i]);
+          az[i] = __ffma2_rn(cj, dx, az[i]);
+          const float2 ci = __fmul2_rn(make_float2(tg[i], tg[i]), rs);
+          bx = __ffma2_rn(ci, dz, bx);
+          bz = __ffma2_rn(ci, dx, bz);
+        }
+        sx.x = __shfl_sync(0xffffffffu, sx.x, nxt);
+        sx.y = __shfl_sync(0xffffffffu, sx.y, nxt);
+        sz.x = __shfl_sync(0xffffffffu, sz.x, nxt);
+        sz.y = __shfl_sync(0xffffffffu, sz.y, nxt);
+        sg.x = __shfl_sync(0xffffffffu, sg.x, nxt);
+        sg.y = __shfl_sync(0xffffffffu, sg.y, nxt);
+        bx.x = __shfl_sync(0xffffffffu, bx.x, nxt);
+        bx.y = __shfl_sync(0xffffffffu, bx.y, nxt);
+        bz.x = __shfl_sync(0xffffffffu, bz.x, nxt);
+        bz.y = __shfl_sync(0xffffffffu, bz.y, nxt);
+      }
+      part[2 * (32 * J0 + lane)] = bx.x;
+      part[2 * (32 * J0 + lane) + 1] = bz.x;
+      part[2 * (32 * J0 + 32 + lane)] = bx.y;
+      part[2 * (32 * J0 + 32 + lane) + 1] = bz.y;
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s += ax[i].x + ax[i].y + az[i].x + az[i].y;
+  if (s == 1.2345f) out[blockIdx.x] = s;
+}
+
 static int g_sms, g_clk_khz;
 
 template <typename F>
@@ -304,6 +367,15 @@ static void run_rotl(float *out, int n, int ctas) {
   report(FOLD ? "rotl_fold" : "rotl", NPK, FOLD, UNR, MAXREG, ctas, 2.0 * grid * threads * 4 * n * reps, ms);
 }
 
+template <int MAXREG, int UNR>
+static void run_rotsp(float *out, int n, int ctas) {
+  const int reps = 20, threads = 128, grid = g_sms * ctas * 4;
+  const size_t smem = n * 16 + n * 8;
+  cudaFuncSetAttribute(rotsp_kernel<MAXREG, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  float ms = time_ms([&] { rotsp_kernel<MAXREG, UNR><<<grid, threads, smem>>>(out, n, reps, 1e-4f); });
+  report("rot_source_packed", 2, 1, UNR, MAXREG, ctas, 2.0 * grid * threads * 4 * n * reps, ms);
+}
+
 int main() {
   cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0);
   cudaDeviceGetAttribute(&g_clk_khz, cudaDevAttrClockRate, 0);
@@ -312,13 +384,11 @@ int main() {
   const int n = 512;
   run_direct<72>(out, n, 7);
   run_rot<1, 1, 72, 4>(out, n, 7);
-  run_rotl<1, 0, 72, 4>(out, n, 7);
-  run_rotl<1, 1, 72, 4>(out, n, 7);
-  run_rotl<2, 0, 72, 2>(out, n, 7);
-  run_rotl<2, 1, 72, 2>(out, n, 7);
-  run_rotl<1, 0, 64, 4>(out, n, 8);
-  run_rotl<1, 0, 72, 8>(out, n, 7);
-  run_rotl<2, 0, 80, 2>(out, n, 6);
+  run_rotsp<72, 2>(out, n, 7);
+  run_rotsp<72, 4>(out, n, 7);
+  run_rotsp<80, 2>(out, n, 6);
+  run_rotsp<64, 2>(out, n, 8);
+  run_rotsp<96, 2>(out, n, 5);
   printf("{\"sms\":%d,\"clk_mhz\":%d}\n", g_sms, g_clk_khz / 1000);
   return 0;
 }
