@@ -170,23 +170,33 @@ int device_sms() {
   return sms;
 }
 
-// Launch shape.  A rollout CTA has NT threads; each holds R register target slots
-// (slot k of warp w = particles 32 (NW k + NW-1-w) .. +31) covering cap + 4 (the
-// largest wake a snapshot may hold), so every particle is a register target.
-// Warp 0 runs the FP64 loads / dynamics / geometry phase after its slots.  NT is
-// the smallest power of two >= 64 (>= the split-sweep chain count when the launch
-// is latency-bound) that still puts >= 24 warps on every SM given how many
-// rollouts each SM receives (4097 rollouts on one GPU -> 128 x 5, 512 per GPU at
-// 8 GPUs -> 256 x 3).  Results do not depend on the shape (canonical reduction
-// orders, see vpm_rollout.cuh).  VPM_SHAPE="nt,r" / VPM_MAXREG override for tuning.
+// Launch shape.  A rollout CTA has NT threads; each holds R register target slots.
+// Caps above 256 use the symmetric-pair sweep with NT = 32 x ceil(cap / 128) (fixed
+// by the cap, below).  Direct sweep (caps <= 256, and VPM_SYM=0): slot k of warp w =
+// particles 32 (NW k + NW-1-w) .. +31, NT x R >= cap + 4 (the largest wake a
+// snapshot may hold), so every particle is a register target; NT is the smallest
+// power of two >= 64 (>= the split-sweep chain count when the launch is
+// latency-bound) that still puts >= 24 warps on every SM given how many rollouts each
+// SM receives.  Results do not depend on the direct shape (canonical reduction
+// orders, see vpm_rollout.cuh).  VPM_SHAPE="nt,r" (direct) / VPM_MAXREG override for
+// tuning.
 Shape pick_shape(int cap, int nb, int rows) {
   const int need = cap + 4;
   const double per_sm = rows > 0 ? (double)rows / device_sms() : 1.0;
+  if (const char *e = getenv("VPM_SHAPE")) {
+    Shape s{0, 0, 0, 64};
+    if (sscanf(e, "%d,%d", &s.nt, &s.r) == 2 && s.nt >= 64 && s.nt <= vpm::NT_MAX &&
+        s.nt % 32 == 0 && s.r >= 1 && s.r <= 8 && s.nt * s.r >= need) {
+      if (const char *m = getenv("VPM_MAXREG")) s.minb = atoi(m);
+      return s;
+    }
+  }
   // Symmetric-pair sweep for caps above 256: T = ceil(cap / 128) warps of 128-particle
   // tiles (vpm_rollout.cuh, sym_sweep).  The shape is a function of the cap alone, so
   // every launch (single step, batch, any shard) of a given cap sums in the same
   // order.  R >= 4 slots per thread (the tile) and >= cap + 4 targets for the direct
-  // fallback of overfull wakes.  VPM_SYM=0 selects the direct sweep (tuning / A-B).
+  // fallback of overfull wakes.  VPM_SYM=0 selects the direct sweep, and an explicit
+  // VPM_SHAPE (above) a direct-sweep shape (tuning / A-B).
   const char *se = getenv("VPM_SYM");
   if (cap > 256 && cap <= 2048 && !(se && atoi(se) == 0)) {
     const int T = (cap + 127) / 128;
@@ -214,14 +224,6 @@ Shape pick_shape(int cap, int nb, int rows) {
     }
     if (const char *m = getenv("VPM_MAXREG")) s.minb = atoi(m);
     return s;
-  }
-  if (const char *e = getenv("VPM_SHAPE")) {
-    Shape s{0, 0, 0, 64};
-    if (sscanf(e, "%d,%d", &s.nt, &s.r) == 2 && s.nt >= 64 && s.nt <= vpm::NT_MAX &&
-        s.nt % 32 == 0 && s.r >= 1 && s.r <= 8 && s.nt * s.r >= need) {
-      if (const char *m = getenv("VPM_MAXREG")) s.minb = atoi(m);
-      return s;
-    }
   }
   Shape best{512, 8, 0, 64};
   if (per_sm <= 8.0) {

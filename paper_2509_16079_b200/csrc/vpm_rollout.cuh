@@ -867,7 +867,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
     // targets), while the advection writes the new wake back into buffer 0.
     float4 *wake = wbuf;
     float4 *wcmp = wbuf + L.capbuf;
-    const bool sym = a.sym && conv && n_live <= 128 * NW;  // uniform over the CTA
+    const bool sym = R >= 4 && a.sym && conv && n_live <= 128 * NW;  // uniform over the CTA
     // the control phase D runs on warp 0, or with the symmetric sweep on the warp the
     // schedule loads least (SYM_DWARP)
     const int dwarp = sym && SYM_DWARP ? NW - 1 : 0;
