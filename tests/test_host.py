@@ -125,3 +125,20 @@ def test_product_package_never_imports_oracle():
                 src = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "liboracle" not in src and "_ref/" not in src, f
+
+
+def test_symmetric_launch_shape_depends_on_the_cap_only():
+    """The symmetric-pair sweep sums in an order fixed by its tile count, so every
+    launch of a cap above 256 -- one step, a 513-row shard, a 4097-row iteration,
+    C5's 16384 rows -- must get the same thread count (32 x ceil(cap / 128)) and at
+    least four target slots per thread (vpm_capi.cu pick_shape).  Runs without a GPU
+    (the SM count defaults to 148)."""
+    import os
+    from paper_2509_16079_b200.device import launch_shape
+    for key in ("VPM_SHAPE", "VPM_SYM", "VPM_MAXREG"):
+        assert key not in os.environ
+    for cap in (257, 300, 512, 640, 1000, 1024, 2048):
+        t_expect = 32 * ((cap + 127) // 128)
+        shapes = {launch_shape(cap, 10, rows)[:2] for rows in (1, 65, 257, 513, 1025, 4097, 16384)}
+        assert {t for t, _ in shapes} == {t_expect}, (cap, shapes)
+        assert all(r >= 4 and t * r >= cap + 4 for t, r in shapes), (cap, shapes)

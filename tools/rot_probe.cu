@@ -67,15 +67,15 @@ __global__ void __maxnreg__(MAXREG) direct_kernel(float *out, int n, int reps, f
   if (s == 1.2345f) out[blockIdx.x] = s;
 }
 
-template <int NPK, int ACC2, int MAXREG, int UNR>
+template <int NPK, int ACC2, int MAXREG, int UNR, int KPT = 2>
 __global__ void __maxnreg__(MAXREG) rot_kernel(float *out, int n, int reps, float rc4) {
   extern __shared__ float4 src[];
   fill(src, n);
   float *part = reinterpret_cast<float *>(src + n);
   const int lane = threadIdx.x & 31;
-  float2 px[2], pz[2], pg[2], qx[2], qz[2];
+  float2 px[KPT], pz[KPT], pg[KPT], qx[KPT], qz[KPT];
 #pragma unroll
-  for (int p = 0; p < 2; ++p) {
+  for (int p = 0; p < KPT; ++p) {
     px[p] = make_float2(-0.013f * (threadIdx.x + p), -0.017f * p);
     pz[p] = make_float2(-0.011f * p, -0.019f * (threadIdx.x & 3));
     pg[p] = make_float2(1e-3f * (p + 1), -1e-3f * (lane & 1));
@@ -105,7 +105,7 @@ __global__ void __maxnreg__(MAXREG) rot_kernel(float *out, int n, int reps, floa
                        sg2 = make_float2(sg[k], sg[k]);
           float2 tx = make_float2(0.f, 0.f), tz = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int p = 0; p < 2; ++p) {
+          for (int p = 0; p < KPT; ++p) {
             const float2 dx = __fadd2_rn(sx2, px[p]);
             const float2 dz = __fadd2_rn(sz2, pz[p]);
             const float2 r2 = __ffma2_rn(dx, dx, __fmul2_rn(dz, dz));
@@ -157,7 +157,7 @@ __global__ void __maxnreg__(MAXREG) rot_kernel(float *out, int n, int reps, floa
   }
   float s = 0.f;
 #pragma unroll
-  for (int p = 0; p < 2; ++p) s += qx[p].x + qx[p].y + qz[p].x + qz[p].y;
+  for (int p = 0; p < KPT; ++p) s += qx[p].x + qx[p].y + qz[p].x + qz[p].y;
   if (s == 1.2345f) out[blockIdx.x] = s;
 }
 
@@ -348,14 +348,15 @@ static void run_direct(float *out, int n, int ctas) {
   report("direct", 0, 0, 8, MAXREG, ctas, (double)grid * threads * 4 * n * reps, ms);
 }
 
-template <int NPK, int ACC2, int MAXREG, int UNR>
+template <int NPK, int ACC2, int MAXREG, int UNR, int KPT = 2>
 static void run_rot(float *out, int n, int ctas) {
   const int reps = 20, threads = 128, grid = g_sms * ctas * 4;
   const size_t smem = n * 16 + n * 8;
-  cudaFuncSetAttribute(rot_kernel<NPK, ACC2, MAXREG, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  float ms = time_ms([&] { rot_kernel<NPK, ACC2, MAXREG, UNR><<<grid, threads, smem>>>(out, n, reps, 1e-4f); });
-  // per lane and step: 4 targets x 1 source = 4 pairs = 8 directed
-  report("rot", NPK, ACC2, UNR, MAXREG, ctas, 2.0 * grid * threads * 4 * n * reps, ms);
+  cudaFuncSetAttribute(rot_kernel<NPK, ACC2, MAXREG, UNR, KPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  float ms = time_ms([&] { rot_kernel<NPK, ACC2, MAXREG, UNR, KPT><<<grid, threads, smem>>>(out, n, reps, 1e-4f); });
+  // per lane and step: 2 KPT targets x 1 source = 2 KPT pairs
+  report(KPT == 2 ? "rot" : (KPT == 3 ? "rot_6targets" : "rot_8targets"), NPK, ACC2, UNR, MAXREG, ctas,
+         2.0 * grid * threads * 2 * KPT * n * reps, ms);
 }
 
 template <int NPK, int FOLD, int MAXREG, int UNR>
@@ -384,11 +385,11 @@ int main() {
   const int n = 512;
   run_direct<72>(out, n, 7);
   run_rot<1, 1, 72, 4>(out, n, 7);
-  run_rotsp<72, 2>(out, n, 7);
-  run_rotsp<72, 4>(out, n, 7);
-  run_rotsp<80, 2>(out, n, 6);
-  run_rotsp<64, 2>(out, n, 8);
-  run_rotsp<96, 2>(out, n, 5);
+  run_rot<1, 1, 80, 4, 3>(out, n, 6);
+  run_rot<1, 1, 88, 4, 3>(out, n, 5);
+  run_rot<1, 1, 96, 4, 3>(out, n, 5);
+  run_rot<1, 1, 96, 2, 4>(out, n, 5);
+  run_rot<1, 1, 104, 2, 4>(out, n, 4);
   printf("{\"sms\":%d,\"clk_mhz\":%d}\n", g_sms, g_clk_khz / 1000);
   return 0;
 }
