@@ -712,9 +712,11 @@ __device__ __forceinline__ int raw_index(int c, const int *holes, int nh) {
 // Source-split sweep for a handful of targets tgt[0..nt) (the nb panel or
 // collocation points): the sources are cut into NSEG fixed segments and every
 // (target, segment) pair is one sequential chain on one thread, stored as
-// red[seg * RS + 2k (+1)] = (sum c d'_z, sum c d'_x); consumers add the segments
-// in order.  The cut depends only on n, so the result does not depend on the CTA
-// shape; no cross-lane reductions are needed.
+// red[(k NSEG + seg) 2 (+1)] = (sum c d'_z, sum c d'_x) -- target-major: consecutive
+// tasks write consecutive float pairs, free of bank conflicts (the segment-major
+// layout cost the 513-row shard 3.7%) -- and consumers add the segments in order.  The
+// cut depends only on n, so the result does not depend on the CTA shape; no
+// cross-lane reductions are needed.
 __device__ __forceinline__ void split_sweep(const float4 *__restrict__ src, int n,
                                             const float2 *tgt, int nt, float rc4, float *red,
                                             int RS, int tid, int nthreads) {
@@ -729,18 +731,17 @@ __device__ __forceinline__ void split_sweep(const float4 *__restrict__ src, int 
       const float4 s = src[j];
       bs_chain(s.x, s.y, s.z, ntx, ntz, rc4, ax, az);
     }
-    red[seg * RS + 2 * k] = ax;
-    red[seg * RS + 2 * k + 1] = az;
+    red[(k * NSEG + seg) * 2] = ax;
+    red[(k * NSEG + seg) * 2 + 1] = az;
   }
 }
 
 // wake velocity at split target k from the per-segment partials (segment order)
-__device__ __forceinline__ void split_result(const float *red, int RS, int nblk, int k, double &ux,
-                                             double &uz) {
+__device__ __forceinline__ void split_result(const float *red, int k, double &ux, double &uz) {
   double sx = 0.0, sz = 0.0;
-  for (int b = 0; b < nblk; ++b) {
-    sx += (double)red[b * RS + 2 * k];
-    sz += (double)red[b * RS + 2 * k + 1];
+  for (int b = 0; b < NSEG; ++b) {
+    sx += (double)red[(k * NSEG + b) * 2];
+    sz += (double)red[(k * NSEG + b) * 2 + 1];
   }
   ux = -sx;
   uz = sz;
@@ -910,7 +911,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           const int p = lane;
           const bool act = p < nb;
           double uxp = 0.0, uzp = 0.0;
-          if (act) split_result(red, RS, NSEG, p, uxp, uzp);
+          if (act) split_result(red, p, uxp, uzp);
           double cum = act ? gam[p] : 0.0, cum_prev = act ? pgp[p] : 0.0;
           for (int o = 1; o < nb; o <<= 1) {
             const double c1 = __shfl_up_sync(0xffffffffu, cum, o);
@@ -941,7 +942,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
         } else {
           for (int p = lane; p < nb; p += 32) {
             double uxp, uzp;
-            split_result(red, RS, NSEG, p, uxp, uzp);
+            split_result(red, p, uxp, uzp);
             double cum = 0.0, cum_prev = 0.0;
             for (int i = 0; i <= p; ++i) { cum += gam[i]; cum_prev += pgp[i]; }
             const double rate = hp ? (cum - cum_prev) * P.inv_dt + dlev : 0.0;
@@ -1203,7 +1204,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
       const double nx = ctl->nx, nz = ctl->nz;
       for (int i = lane; i < nb; i += 32) {
         double uxw, uzw;
-        split_result(red, RS, NSEG, i, uxw, uzw);
+        split_result(red, i, uxw, uzw);
         const int ri = (shed && rev) ? i : i + 1;
         const double px = cx[ri], pz = cz[ri];
         const double svx = vx + om * (-(pz - rz)), svz = vz + om * (px - rx);
