@@ -678,7 +678,10 @@ def run_ours(args):
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": read_traffic(),
-                     "kernel": f"rollout_kernel<{nt},{r}> (one CTA per rollout, {smem} B smem)",
+                     "kernel": f"rollout_kernel<{nt},{r}> (one CTA per rollout, {smem} B smem, "
+                               + ("symmetric-pair sweep: each wake pair once for both directions, "
+                                  f"{nt // 32} tiles of 128 particles)"
+                                  if CAP > 256 and os.environ.get("VPM_SYM", "1") != "0" else "direct sweep)"),
                      "flop_per_launch": flops_per_launch,
                      "kernel_ms": kern_ms_max,
                      "peak_source": f"max(FFMA probe {peak_meas:.1f}, spec 148x128x2x1.965GHz "
