@@ -83,26 +83,6 @@ constexpr int WAKE_PAD = 8;    // wake slots beyond cap (reference buffers hold 
 #ifndef VPM_D_PASS
 #define VPM_D_PASS 1
 #endif
-#ifndef VPM_SYM_NP2_K2
-#define VPM_SYM_NP2_K2 0
-#endif
-constexpr bool SYM_NP2_K2 = VPM_SYM_NP2_K2;  // two packets per rotation also for both target pairs
-#ifndef VPM_SYM_INTRA_DIRECT
-#define VPM_SYM_INTRA_DIRECT 1
-#endif
-#ifndef VPM_SYM_SPLIT_DIRECT
-#define VPM_SYM_SPLIT_DIRECT 0
-#endif
-#ifndef VPM_SYM_FOLD
-#define VPM_SYM_FOLD 0
-#endif
-constexpr int SYM_FOLD = VPM_SYM_FOLD;
-#ifndef VPM_SYM_DWARP
-#define VPM_SYM_DWARP 1
-#endif
-constexpr bool SYM_DWARP = VPM_SYM_DWARP;  // reaction folded to scalars: 0 never, 1 one target pair, 2 always
-constexpr bool SYM_INTRA_DIRECT = VPM_SYM_INTRA_DIRECT;  // own tile swept direct (no intra rotation)
-constexpr bool SYM_SPLIT_DIRECT = VPM_SYM_SPLIT_DIRECT;  // tile pair (w, w+T/2) directed, both sides
 constexpr int SWEEP_UNROLL = VPM_SWEEP_UNROLL;  // sources per sweep-loop trip
 constexpr int D_PASS = VPM_D_PASS;  // warp 0 runs its control phase after (1) / before (0) its sweep
 constexpr bool SLOT_REV = VPM_SLOT_REV;  // last warp takes the odd 32-particle block, not warp 0
@@ -390,10 +370,9 @@ __device__ __noinline__ void sweep_dispatch(int kw, const float4 *src, int n, co
 // 2 x (8 + 1) for the two directed interactions.  The CTA has T warps; warp w owns the
 // tile of particles 128 w + 32 k + lane (slot k = 0..3, held as the packed slot pairs
 // (0,1) and (2,3)).  Pairs are covered as
-//   - the two diagonal super-blocks (slots 0,1 x particles of slots 0,1; 2,3 x 2,3):
-//     direct, sources as shared-memory broadcasts;
-//   - slots (0,1) x slots 2 and 3 of the same tile: lane rotation (below), the
-//     reaction comes home to the owning lane;
+//   - the own tile (and the previous bound row): direct, all four slots per
+//     shared-memory broadcast source (rotating the tile's slots 2,3 past slots 0,1
+//     instead measured slower: with one target pair per step the shuffles bound it);
 //   - tile pairs (w, w+d), d = 1..(T-1)/2: warp w rotates every 32-particle block of
 //     tile w+d through its lanes; the reactions go to a shared-memory buffer that the
 //     owning warp adds after a barrier; for even T the pair (w, w+T/2) is split by
@@ -428,32 +407,6 @@ __device__ __forceinline__ void sym_direct(const float4 *__restrict__ src, int j
   }
 }
 
-// the two diagonal super-blocks at once: pair 0 vs sources [b0, b0 + n0), pair 1 vs
-// [b1, b1 + n1), n1 <= n0 (two independent chains per iteration)
-__device__ __forceinline__ void sym_direct_diag(const float4 *__restrict__ src, int b0, int n0, int b1, int n1,
-                                                const float2 *px, const float2 *pz, float2 *qx, float2 *qz,
-                                                float2 rc) {
-#pragma unroll 4
-  for (int j = 0; j < n1; ++j) {
-    const float4 s0 = src[b0 + j], s1 = src[b1 + j];
-    const float2 sx[2] = {make_float2(s0.x, s0.x), make_float2(s1.x, s1.x)};
-    const float2 sz[2] = {make_float2(s0.y, s0.y), make_float2(s1.y, s1.y)};
-    const float2 sg[2] = {make_float2(s0.z, s0.z), make_float2(s1.z, s1.z)};
-#pragma unroll
-    for (int p = 0; p < 2; ++p) {
-      const float2 dx = __fadd2_rn(sx[p], px[p]);
-      const float2 dz = __fadd2_rn(sz[p], pz[p]);
-      const float2 r2 = __ffma2_rn(dx, dx, __fmul2_rn(dz, dz));
-      const float2 q = __ffma2_rn(r2, r2, rc);
-      const float2 rs = make_float2(rsqrt_mufu(q.x), rsqrt_mufu(q.y));
-      const float2 c = __fmul2_rn(sg[p], rs);
-      qx[p] = __ffma2_rn(c, dz, qx[p]);
-      qz[p] = __ffma2_rn(c, dx, qz[p]);
-    }
-  }
-  sym_direct<1>(src, b0 + n1, b0 + n0, px, pz, qx, qz, rc);
-}
-
 // NK packets (sx, sz, sg) rotated together through the lanes against NP packed
 // target pairs (px, pz = negated target coordinates, pg = negated target Gamma/2pi);
 // per step every packet meets the targets in packet order.  Returns the reaction on
@@ -462,53 +415,6 @@ template <int NP, int NK>
 __device__ __forceinline__ void sym_rotate(float *sx, float *sz, float *sg, const float2 *px, const float2 *pz,
                                            const float2 *pg, float2 *qx, float2 *qz, float2 rc, int nxt,
                                            float *rbx, float *rbz) {
-  // FOLD: the reaction travels as scalars (2 shuffles instead of 4 per packet and step,
-  // 2 extra FADD): shuffles share the SM-wide L1 data pipe with the shared-memory loads
-  constexpr bool FOLD = SYM_FOLD >= 2 || (SYM_FOLD == 1 && NP == 1);
-  if constexpr (FOLD) {
-    float fx[NK], fz[NK];
-#pragma unroll
-    for (int k = 0; k < NK; ++k) fx[k] = fz[k] = 0.f;
-#pragma unroll(NK == 1 ? 4 : 2)
-    for (int r = 0; r < 32; ++r) {
-#pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        const float2 sx2 = make_float2(sx[k], sx[k]), sz2 = make_float2(sz[k], sz[k]),
-                     sg2 = make_float2(sg[k], sg[k]);
-        float2 tx, tz;
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          const float2 dx = __fadd2_rn(sx2, px[p]);
-          const float2 dz = __fadd2_rn(sz2, pz[p]);
-          const float2 r2 = __ffma2_rn(dx, dx, __fmul2_rn(dz, dz));
-          const float2 q = __ffma2_rn(r2, r2, rc);
-          const float2 rs = make_float2(rsqrt_mufu(q.x), rsqrt_mufu(q.y));
-          const float2 cj = __fmul2_rn(sg2, rs);
-          qx[p] = __ffma2_rn(cj, dz, qx[p]);
-          qz[p] = __ffma2_rn(cj, dx, qz[p]);
-          const float2 ci = __fmul2_rn(pg[p], rs);
-          tx = p == 0 ? __fmul2_rn(ci, dz) : __ffma2_rn(ci, dz, tx);
-          tz = p == 0 ? __fmul2_rn(ci, dx) : __ffma2_rn(ci, dx, tz);
-        }
-        fx[k] += tx.x + tx.y;
-        fz[k] += tz.x + tz.y;
-      }
-#pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        sx[k] = __shfl_sync(0xffffffffu, sx[k], nxt);
-        sz[k] = __shfl_sync(0xffffffffu, sz[k], nxt);
-        sg[k] = __shfl_sync(0xffffffffu, sg[k], nxt);
-        fx[k] = __shfl_sync(0xffffffffu, fx[k], nxt);
-        fz[k] = __shfl_sync(0xffffffffu, fz[k], nxt);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < NK; ++k) {
-      rbx[k] = fx[k];
-      rbz[k] = fz[k];
-    }
-    return;
-  }
   float2 bx[NK], bz[NK];
 #pragma unroll
   for (int k = 0; k < NK; ++k) bx[k] = bz[k] = make_float2(0.f, 0.f);
@@ -577,21 +483,10 @@ __device__ __noinline__ void sym_sweep(const float4 *__restrict__ wb, float2 *rb
     qz[p] = make_float2(0.f, 0.f);
   }
   const bool act0 = base < nl, act1 = base + 64 < nl;
-  // previous bound row and the diagonal super-blocks, direct
-  if (act1 && SYM_INTRA_DIRECT) {
+  // previous bound row and the own tile, direct (all four slots per broadcast source)
+  if (act1) {
     sym_direct<2>(psrc, 0, n_prev, px, pz, qx, qz, rc);
     sym_direct<2>(wb, base, min(base + 128, nl), px, pz, qx, qz, rc);
-  } else if (act1) {
-    sym_direct<2>(psrc, 0, n_prev, px, pz, qx, qz, rc);
-    sym_direct_diag(wb, base, 64, base + 64, min(64, nl - base - 64), px, pz, qx, qz, rc);
-    // slots (0,1) x the particles of slots 2 and 3 (two packets together)
-    float sx[2] = {-px[1].x, -px[1].y}, sz[2] = {-pz[1].x, -pz[1].y}, sg[2] = {-pg[1].x, -pg[1].y};
-    float rbx[2], rbz[2];
-    sym_rotate<1, 2>(sx, sz, sg, px, pz, pg, qx, qz, rc, nxt, rbx, rbz);
-    qx[1].x += rbx[0];
-    qz[1].x += rbz[0];
-    qx[1].y += rbx[1];
-    qz[1].y += rbz[1];
   } else if (act0) {
     sym_direct<1>(psrc, 0, n_prev, px, pz, qx, qz, rc);
     sym_direct<1>(wb, base, min(base + 64, nl), px, pz, qx, qz, rc);
@@ -603,13 +498,12 @@ __device__ __noinline__ void sym_sweep(const float4 *__restrict__ wb, float2 *rb
     int m = m0;
     while (m < m1 && 128 * v + 32 * m < nl) {
       const int j = 128 * v + 32 * m;
-      if ((np == 1 || SYM_NP2_K2) && m + 1 < m1 && j + 32 < nl) {
+      if (np == 1 && m + 1 < m1 && j + 32 < nl) {
         const float4 s0 = j + lane < nl ? wb[j + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
         const float4 s1 = j + 32 + lane < nl ? wb[j + 32 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
         float sx[2] = {s0.x, s1.x}, sz[2] = {s0.y, s1.y}, sg[2] = {s0.z, s1.z};
         float rbx[2], rbz[2];
-        if (SYM_NP2_K2 && np == 2) sym_rotate<2, 2>(sx, sz, sg, px, pz, pg, qx, qz, rc, nxt, rbx, rbz);
-        else sym_rotate<1, 2>(sx, sz, sg, px, pz, pg, qx, qz, rc, nxt, rbx, rbz);
+        sym_rotate<1, 2>(sx, sz, sg, px, pz, pg, qx, qz, rc, nxt, rbx, rbz);
         dst[32 * m + lane] = make_float2(rbx[0], rbz[0]);
         dst[32 * m + 32 + lane] = make_float2(rbx[1], rbz[1]);
         m += 2;
@@ -642,12 +536,7 @@ __device__ __noinline__ void sym_sweep(const float4 *__restrict__ wb, float2 *rb
     const int u = w - d >= 0 ? w - d : w - d + T;  // the warp that rotated this tile
     if (act0 && 128 * u < nl) receive(rb + 256 * w + 128 * (d & 1), 0);
   }
-  if (T >= 2 && (T & 1) == 0 && SYM_SPLIT_DIRECT) {
-    // tile pair (w, w+T/2) directed from both sides: no reactions, no barrier
-    const int v = w < (T >> 1) ? w + (T >> 1) : w - (T >> 1);
-    if (act1) sym_direct<2>(wb, 128 * v, min(128 * v + 128, nl), px, pz, qx, qz, rc);
-    else if (act0) sym_direct<1>(wb, 128 * v, min(128 * v + 128, nl), px, pz, qx, qz, rc);
-  } else if (T >= 2 && (T & 1) == 0) {
+  if (T >= 2 && (T & 1) == 0) {
     const int d = T >> 1;
     if (w < d) {  // slots 0,1 x all of tile w+d
       if (act0) sweep_blocks(w + d, 0, 4, 1, rb + 256 * (w + d) + 128 * (d & 1));
@@ -869,9 +758,9 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
     float4 *wake = wbuf;
     float4 *wcmp = wbuf + L.capbuf;
     const bool sym = R >= 4 && a.sym && conv && n_live <= 128 * NW;  // uniform over the CTA
-    // the control phase D runs on warp 0, or with the symmetric sweep on the warp the
-    // schedule loads least (SYM_DWARP)
-    const int dwarp = sym && SYM_DWARP ? NW - 1 : 0;
+    // the control phase D runs on warp 0, or with the symmetric sweep on the last warp
+    // (warp 0 runs E)
+    const int dwarp = sym ? NW - 1 : 0;
 
     // ---------------- P1: wake velocity at the panels of step t-1 (its loads),
     // source-split over all warps.  (Carrying the 10 panel targets in one warp's
