@@ -376,6 +376,8 @@ struct vpm_plan {
   cudaStream_t hstream = nullptr;
   void *hscratch = nullptr;
   size_t hscratch_len = 0;
+  void *hpin = nullptr;  // pinned host staging of the small inputs / outputs
+  size_t hpin_len = 0;
 };
 
 static Args base_args(const vpm_plan *p) {
@@ -496,6 +498,7 @@ void vpm_plan_destroy(vpm_plan *p) {
   cudaFree(p->d_ticket);
   cudaFree(p->d_rec);
   cudaFree(p->hscratch);
+  if (p->hpin) cudaFreeHost(p->hpin);
   if (p->hstream) cudaStreamDestroy(p->hstream);
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
   delete p;
@@ -875,33 +878,46 @@ int vpm_mppi_optimize_host(vpm_plan *p, const double *x0, double *u_star, const 
     off += bytes;
     return r;
   };
-  double *d_x0 = (double *)take(7 * sizeof(double));
-  double *d_u = (double *)take((T + 1) * sizeof(double));
+  // the small inputs x0 | u* | q | x_perch as one block (one staged copy)
+  const size_t nsmall = 7 + (size_t)T + 7 + 7;
+  double *d_small = (double *)take(nsmall * sizeof(double));
+  double *d_x0 = d_small, *d_u = d_small + 7, *d_q = d_u + T, *d_xp = d_q + 7;
   double *d_noise = (double *)take((nn + 1) * sizeof(double));
-  double *d_q = (double *)take(7 * sizeof(double));
-  double *d_xp = (double *)take(7 * sizeof(double));
   double *d_cost = (double *)take(B * sizeof(double));
   double *d_part = (double *)take((T + 2) * sizeof(double));
   int32_t *d_flag = (int32_t *)take((iters + 1) * sizeof(int32_t));
-  CK(cudaMemcpyAsync(d_x0, x0, 7 * sizeof(double), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_u, u_star, T * sizeof(double), cudaMemcpyHostToDevice, st));
+  // pinned staging [small inputs | u* out | flags out]: from pageable sources every
+  // small copy would be a synchronous staged transfer
+  const size_t pin_need = sizeof(double) * (nsmall + T) + sizeof(int32_t) * (iters + 1);
+  if (p->hpin_len < pin_need) {
+    if (p->hpin) cudaFreeHost(p->hpin);
+    p->hpin = nullptr;
+    p->hpin_len = 0;
+    CK(cudaMallocHost(&p->hpin, pin_need));
+    p->hpin_len = pin_need;
+  }
+  double *h_small = (double *)p->hpin, *h_u = h_small + nsmall;
+  int32_t *h_flags = (int32_t *)(h_u + T);
+  std::memcpy(h_small, x0, 7 * sizeof(double));
+  std::memcpy(h_small + 7, u_star, T * sizeof(double));
+  std::memcpy(h_small + 7 + T, q, 7 * sizeof(double));
+  std::memcpy(h_small + 14 + T, x_perch, 7 * sizeof(double));
+  CK(cudaMemcpyAsync(d_small, h_small, nsmall * sizeof(double), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_noise, noise, nn * sizeof(double), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_q, q, 7 * sizeof(double), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_xp, x_perch, 7 * sizeof(double), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(d_flag, 0, iters * sizeof(int32_t) + 4, st));
   int rc = VPM_OK;
   for (int it = 0; it < iters && rc == VPM_OK; ++it)
     rc = vpm_mppi_iteration(p, d_x0, d_u, d_noise + (size_t)it * K * T, sigma, B, T, temperature, d_q,
                             d_xp, d_cost, d_part, d_flag + it, 0, st);
-  std::vector<int32_t> flags(iters > 0 ? iters : 1, 0);
   if (rc == VPM_OK) {
-    CK(cudaMemcpyAsync(u_star, d_u, T * sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (iters > 0) CK(cudaMemcpyAsync(flags.data(), d_flag, iters * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_u, d_u, T * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (iters > 0) CK(cudaMemcpyAsync(h_flags, d_flag, iters * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   }
   CK(cudaStreamSynchronize(st));
   if (rc) return rc;
+  std::memcpy(u_star, h_u, T * sizeof(double));
   for (int it = 0; it < iters; ++it)
-    if (flags[it]) {
+    if (h_flags[it]) {
       g_err = "all sampled rollouts failed (infinite cost)";
       return VPM_ERR_ALLFAIL;
     }
