@@ -718,3 +718,31 @@ def test_symmetric_tiles_vs_oracle(torch_cuda, oracle_core, cap, n0):
         assert rc == res.status[k]
         if rc == 0:
             np.testing.assert_array_equal(traj, res.trajectories[k])
+
+
+@pytest.mark.parametrize("cap,n0", [(60, 40), (512, 500)])
+def test_failure_time_wake_vs_oracle(torch_cuda, oracle_core, cap, n0):
+    """A rollout that leaves the envelope mid-horizon returns the wake of its
+    failure time (the reference's run_rollout semantics, _core.pyx:465-491): the
+    direct sweep (cap 60) and the symmetric sweep (cap 512), whose advection has
+    already rewritten the wake buffer when the control phase detects the failure, so
+    the dump comes from the compacted copy."""
+    from paper_2509_16079_b200 import config, rollout, vpm
+    rng = np.random.default_rng(cap)
+    v = config.VpmConfig(particle_cap=cap)
+    eng = rollout.Engine(v, config.GliderParams())
+    fl = vpm.FluidState.empty(v)
+    fl.wake_pos[:n0] = rng.normal(0.0, 0.5, (n0, 2)) - np.array([3.0, 0.0])
+    fl.wake_gamma[:n0] = rng.normal(0.0, 0.02, n0)
+    fl.wake_age[:n0] = rng.integers(0, 300, n0)
+    fl.n_wake = n0
+    x0 = np.array([0.0, 0.0, 0.3, 0.0, 7.0, 30.0, 0.0])  # leaves the envelope after 3-7 steps
+    ctrl = np.full(20, 15.0)
+    rc, _, fl_g = eng.rollout(x0, ctrl, fl)
+    rc_o, _, flat_o = oracle_core.rollout(x0, ctrl, *fl.flat(), eng.iparams, eng.fparams, False, True)
+    assert rc == rc_o and 2 < rc < 20, (rc, rc_o)
+    n = flat_o[3]
+    assert fl_g.n_wake == n and (fl_g.ring_a, fl_g.ring_b) == (flat_o[4], flat_o[5])
+    np.testing.assert_array_equal(fl_g.wake_age[:n], flat_o[2][:n])
+    assert_close(fl_g.wake_pos[:n], flat_o[0][:n], "wake_pos", what=f"cap {cap} failure-time wake")
+    assert_close(fl_g.wake_gamma[:n], flat_o[1][:n], "wake_gamma", what=f"cap {cap} failure-time gamma")
