@@ -706,6 +706,14 @@ def test_symmetric_tiles_vs_oracle(torch_cuda, oracle_core, cap, n0):
                      diagnostics=True)
     torch.cuda.synchronize()
     gpu = {k: t.cpu().numpy() for k, t in out.items()}
+    # repeated launches are bitwise identical (a shared-memory race in the tile
+    # schedule would show up as run-to-run differences)
+    for _ in range(3):
+        again = plan.batch(torch.as_tensor(X0, device=dev), T, controls=torch.as_tensor(ctrl, device=dev), rows=B,
+                           diagnostics=True)
+        torch.cuda.synchronize()
+        for k, t in again.items():
+            np.testing.assert_array_equal(t.cpu().numpy(), gpu[k])
     d = oracle_core.batch_rollout_diag(X0, ctrl, *fl.flat(), eng.iparams, eng.fparams, record=True)
     ok = _check_decisions(gpu, d, f"cap {cap}, wake {n0}")
     assert ok.sum() >= 3

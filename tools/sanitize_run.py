@@ -28,6 +28,21 @@ for name, K, H in (("scenario_C4.npz", 3, 3), ("scenario_C3.npz", 3, 4), ("scena
                      record=True, diagnostics=True)
     torch.cuda.synchronize()
     print(name, out["status"].cpu().numpy())
+# the symmetric sweep on odd / even tile counts with partial tiles (caps 640, 1000) and
+# an overfull snapshot (direct fallback for the first step)
+from paper_2509_16079_b200 import config  # noqa: E402
+for cap, n0 in ((640, 600), (1000, 900), (512, 516)):
+    rng = np.random.default_rng(cap)
+    v = config.VpmConfig(particle_cap=cap)
+    ip, fp = config.pack_params(v, config.GliderParams())
+    p5 = DevicePlan(ip, fp)
+    wp = rng.normal(0.0, 0.5, (n0, 2)) - np.array([3.0, 0.0])
+    p5.set_fluid((wp, rng.normal(0.0, 0.02, n0), rng.integers(0, 300, n0), n0, -1, -1, np.zeros((10, 2)),
+                  np.zeros(10), 0, 0.0, np.zeros(10)))
+    ctrl = f64(np.clip(rng.normal(-6.0, 3.0, (2, 3)), -15, 15))
+    out = p5.batch(f64([0.0, 0.0, 0.3, 0.0, 7.0, 0.0, 0.0]), 3, controls=ctrl, rows=2, diagnostics=True)
+    torch.cuda.synchronize()
+    print("cap", cap, out["status"].cpu().numpy())
 cfg = ExperimentConfig()
 eng = rollout.Engine.from_config(cfg)
 fl = vpm.FluidState.empty(cfg.vpm)
