@@ -877,9 +877,11 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           bool fin = true;
 #pragma unroll
           for (int i = 0; i < 7; ++i) fin = fin && isfinite(xn[i]);
+          // lane i stores component i: a select chain, not a 7-way divergent switch
+          double xl = xn[0];
 #pragma unroll
-          for (int i = 0; i < 7; ++i)
-            if (lane == i) ctl->x[i] = xn[i];
+          for (int i = 1; i < 7; ++i) xl = lane == i ? xn[i] : xl;
+          if (lane < 7) ctl->x[lane] = xl;
           if (lane == 0) {
             bool failed = false;
             if (!fin) {
