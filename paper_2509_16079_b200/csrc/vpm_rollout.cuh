@@ -1258,18 +1258,37 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           }
         }
         // sort holes ascending, zero their circulation, remap the ring indices
-        for (int i = 1; i < nholes; ++i) {
-          const int v = hl[i];
-          int j = i - 1;
-          while (j >= 0 && hl[j] > v) { hl[j + 1] = hl[j]; --j; }
-          hl[j + 1] = v;
-        }
-        __syncwarp();
-        if (lane < nholes) wake[hl[lane]].z = 0.f;
         int ra2 = ra, rb2 = rb;
-        for (int h = 0; h < nholes; ++h) {
-          if (ra >= 0 && hl[h] < ra) --ra2;
-          if (rb >= 0 && hl[h] < rb) --rb2;
+        if constexpr (R < 4) {
+          // lane-distributed: lane j holds hole j, its rank among the (distinct) holes
+          // is its sorted position (small-cap kernels; the array form below is kept for
+          // the large ones, see the merge selection above)
+          int hv = -1;
+#pragma unroll
+          for (int h = 0; h < HOLES_MAX; ++h)
+            if (h < nholes && lane == h) hv = hl[h];
+          int rank = 0;
+          for (int k = 0; k < nholes; ++k) rank += __shfl_sync(0xffffffffu, hv, k) < hv;
+          __syncwarp();
+          if (lane < nholes) {
+            wake[hv].z = 0.f;
+            ctl->holes[rank] = hv;
+          }
+          if (ra >= 0) ra2 = ra - __popc(__ballot_sync(0xffffffffu, lane < nholes && hv < ra));
+          if (rb >= 0) rb2 = rb - __popc(__ballot_sync(0xffffffffu, lane < nholes && hv < rb));
+        } else {
+          for (int i = 1; i < nholes; ++i) {
+            const int v = hl[i];
+            int j = i - 1;
+            while (j >= 0 && hl[j] > v) { hl[j + 1] = hl[j]; --j; }
+            hl[j + 1] = v;
+          }
+          __syncwarp();
+          if (lane < nholes) wake[hl[lane]].z = 0.f;
+          for (int h = 0; h < nholes; ++h) {
+            if (ra >= 0 && hl[h] < ra) --ra2;
+            if (rb >= 0 && hl[h] < rb) --rb2;
+          }
         }
         const int n_live_next = n_now - nholes;
         // previous bound row: sources of the next convection sweep, and the
@@ -1286,7 +1305,8 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           ctl->n_raw = n_now;
           ctl->n_live = n_live_next;
           ctl->n_holes = nholes;
-          for (int h = 0; h < nholes; ++h) ctl->holes[h] = hl[h];
+          if constexpr (R >= 4)
+            for (int h = 0; h < nholes; ++h) ctl->holes[h] = hl[h];
           ctl->ring_a = ra2;
           ctl->ring_b = rb2;
           ctl->mcnt = min(MC, max(0, n_live_next + 3 - P.cap));
