@@ -1024,20 +1024,17 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
           if (lane == 0) kblk[slot_base(k) >> 5] = g;
         }
       }
+      // keys are unique (the particle index is in the low bits), so the winner is
+      // cleared by value: predicated selects, not a divergent switch on its slot
       const int mc = ctl->mcnt;
       for (int r = 0; r < mc; ++r) {
         unsigned best = 0u;
-        int bi = -1;
 #pragma unroll
-        for (int k = 0; k < R; ++k)
-          if (keys[k] > best) { best = keys[k]; bi = k; }
+        for (int k = 0; k < R; ++k) best = max(best, keys[k]);
         const unsigned w = __reduce_max_sync(0xffffffffu, best);
         if (lane == 0) cand[warp * MC + r] = w;
-        if (w != 0u && best == w) {
 #pragma unroll
-          for (int k = 0; k < R; ++k)
-            if (k == bi) keys[k] = 0u;
-        }
+        for (int k = 0; k < R; ++k) keys[k] = (w != 0u && keys[k] == w) ? 0u : keys[k];
       }
     }
       PHASE_MARK(3);
