@@ -12,4 +12,7 @@ Nothing in ``paper_2509_16079_b200`` imports this package.  Only ``tests/``,
   ``policy.py:66-266`` driven by :mod:`oracle.core`.
 * :mod:`oracle.refcore` -- loader for ``oracle/_ref/_core*.so``, the reference's
   own Cython core compiled by ``oracle/build_ref.sh``.
+* :mod:`oracle.refpkg` -- imports the unmodified reference package staged under
+  ``oracle/_ref/pkg`` and installs a stepping module as its compiled core (the
+  drop-in tests run the reference's own API on the CUDA backend).
 """

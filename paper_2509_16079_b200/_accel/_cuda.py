@@ -13,7 +13,7 @@ from __future__ import annotations
 import numpy as np
 
 from .. import _lib
-from .._lib import _D, _I64, as_f64, as_i64, check, fluid_out, fluid_struct, fluid_tuple, ptr
+from .._lib import _D, _I64, addr, as_f64, as_i64, check, fluid_out, fluid_struct, fluid_tuple, ptr
 
 
 def step(x, u, wake_pos, wake_gamma, wake_age, n_wake, ring_a, ring_b, prev_pos, prev_gamma,
@@ -22,13 +22,13 @@ def step(x, u, wake_pos, wake_gamma, wake_age, n_wake, ring_a, ring_b, prev_pos,
     ip, fp = as_i64(iparams), as_f64(fparams)
     f, keep = fluid_struct(wake_pos, wake_gamma, wake_age, n_wake, ring_a, ring_b, prev_pos,
                            prev_gamma, n_prev, prev_lev, ema)
-    xs = as_f64(x).copy()
-    fw = np.zeros(2)
-    mw = np.zeros(1)
-    fo, bufs = fluid_out(int(ip[1]), int(ip[0]))
-    rc = check(_lib.lib().vpm_step(ptr(xs, _D), float(u), f, ptr(ip, _I64), ptr(fp, _D),
-                                   int(bool(integrate)), ptr(fw, _D), ptr(mw, _D), fo), "step")
-    return rc, xs, fw, float(mw[0]), fluid_tuple(bufs)
+    # x (7) | fw (2) | mw (1) lead the output fluid's block: one fresh allocation
+    fo, bufs = fluid_out(int(ip[1]), int(ip[0]), head=10)
+    h, base = bufs["head"], bufs["base"]
+    h[:7] = as_f64(x).reshape(7)
+    rc = check(_lib.lib().vpm_step(base, float(u), f, addr(ip), addr(fp), int(bool(integrate)), base + 56,
+                                   base + 72, fo), "step")
+    return rc, h[0:7], h[7:9], float(h[9]), fluid_tuple(bufs)
 
 
 def rollout(x0, controls, wake_pos, wake_gamma, wake_age, n_wake, ring_a, ring_b, prev_pos,

@@ -58,15 +58,19 @@ _I32 = C.POINTER(C.c_int32)
 _U64 = C.POINTER(C.c_uint64)
 
 
+# Pointer fields are declared c_void_p (the same ABI as the typed pointers of
+# include/vpm_b200.h) so they take plain integer addresses: numpy's typed
+# ``ctypes.data_as`` costs microseconds per pointer on the per-step host path.
 class VpmFluid(C.Structure):
-    _fields_ = [("wake_pos", _D), ("wake_gamma", _D), ("wake_age", _I64), ("n_wake", C.c_int32),
-                ("ring_a", C.c_int32), ("ring_b", C.c_int32), ("prev_pos", _D),
-                ("prev_gamma", _D), ("n_prev", C.c_int32), ("prev_lev", C.c_double), ("ema", _D)]
+    _fields_ = [("wake_pos", C.c_void_p), ("wake_gamma", C.c_void_p), ("wake_age", C.c_void_p),
+                ("n_wake", C.c_int32), ("ring_a", C.c_int32), ("ring_b", C.c_int32), ("prev_pos", C.c_void_p),
+                ("prev_gamma", C.c_void_p), ("n_prev", C.c_int32), ("prev_lev", C.c_double), ("ema", C.c_void_p)]
 
 
 class VpmFluidOut(C.Structure):
-    _fields_ = [("wake_pos", _D), ("wake_gamma", _D), ("wake_age", _I64), ("scalars", _I32),
-                ("prev_pos", _D), ("prev_gamma", _D), ("prev_lev", _D), ("ema", _D)]
+    _fields_ = [("wake_pos", C.c_void_p), ("wake_gamma", C.c_void_p), ("wake_age", C.c_void_p),
+                ("scalars", C.c_void_p), ("prev_pos", C.c_void_p), ("prev_gamma", C.c_void_p),
+                ("prev_lev", C.c_void_p), ("ema", C.c_void_p)]
 
 
 class VpmBatchOut(C.Structure):
@@ -96,7 +100,7 @@ def lib():
             raise CudaBackendError(f"cannot load {LIB_PATH}: {err}") from err
         vp = C.c_void_p
         sig = {
-            "vpm_step": (C.c_int, [_D, C.c_double, C.POINTER(VpmFluid), _I64, _D, C.c_int, _D, _D,
+            "vpm_step": (C.c_int, [vp, C.c_double, C.POINTER(VpmFluid), vp, vp, C.c_int, vp, vp,
                                    C.POINTER(VpmFluidOut)]),
             "vpm_rollout": (C.c_int64, [_D, _D, C.c_int, C.POINTER(VpmFluid), _I64, _D, _D,
                                         C.POINTER(VpmFluidOut)]),
@@ -189,6 +193,11 @@ def ptr(a: np.ndarray, t):
     return a.ctypes.data_as(t)
 
 
+def addr(a: np.ndarray) -> int:
+    """Integer address of a contiguous array (for c_void_p arguments / fields)."""
+    return a.ctypes.data
+
+
 def as_f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
@@ -203,19 +212,27 @@ def fluid_struct(wake_pos, wake_gamma, wake_age, n_wake, ring_a, ring_b, prev_po
     Returns (struct, keepalive)."""
     keep = (as_f64(wake_pos), as_f64(wake_gamma), as_i64(wake_age), as_f64(prev_pos),
             as_f64(prev_gamma), as_f64(ema))
-    f = VpmFluid(ptr(keep[0], _D), ptr(keep[1], _D), ptr(keep[2], _I64), int(n_wake), int(ring_a),
-                 int(ring_b), ptr(keep[3], _D), ptr(keep[4], _D), int(n_prev), float(prev_lev),
-                 ptr(keep[5], _D))
+    f = VpmFluid(addr(keep[0]), addr(keep[1]), addr(keep[2]), int(n_wake), int(ring_a), int(ring_b),
+                 addr(keep[3]), addr(keep[4]), int(n_prev), float(prev_lev), addr(keep[5]))
     return f, keep
 
 
-def fluid_out(cap: int, nb: int):
-    bufs = dict(wp=np.zeros((cap + 4, 2)), wg=np.zeros(cap + 4), wa=np.zeros(cap + 4, np.int64),
-                sc=np.zeros(4, np.int32), pp=np.zeros((nb, 2)), pg=np.zeros(nb), pl=np.zeros(1),
-                em=np.zeros(nb))
-    s = VpmFluidOut(ptr(bufs["wp"], _D), ptr(bufs["wg"], _D), ptr(bufs["wa"], _I64),
-                    ptr(bufs["sc"], _I32), ptr(bufs["pp"], _D), ptr(bufs["pg"], _D),
-                    ptr(bufs["pl"], _D), ptr(bufs["em"], _D))
+def fluid_out(cap: int, nb: int, head: int = 0):
+    """Output fluid buffers as views of ONE fresh float64 block (one address lookup):
+    [head doubles | wake_pos 2(cap+4) | wake_gamma | wake_age (int64 view) | scalars
+    (4 x int32 view) | prev_pos 2 nb | prev_gamma | prev_lev | ema]; ``bufs["head"]``
+    is the caller's leading space, ``bufs["base"]`` the block's address."""
+    c4 = cap + 4
+    sizes = (head, 2 * c4, c4, c4, 2, 2 * nb, nb, 1, nb)
+    offs = np.cumsum((0,) + sizes)
+    block = np.zeros(int(offs[-1]))
+    base = addr(block)
+    o = [int(v) for v in offs]
+    bufs = dict(head=block[o[0]:o[1]], wp=block[o[1]:o[2]].reshape(c4, 2), wg=block[o[2]:o[3]],
+                wa=block[o[3]:o[4]].view(np.int64), sc=block[o[4]:o[5]].view(np.int32),
+                pp=block[o[5]:o[6]].reshape(nb, 2), pg=block[o[6]:o[7]], pl=block[o[7]:o[8]],
+                em=block[o[8]:o[9]], base=base)
+    s = VpmFluidOut(*(base + 8 * o[i] for i in range(1, 9)))
     return s, bufs
 
 
