@@ -141,7 +141,7 @@ def lib():
             "vpm_plan_cloud": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_double, C.c_int, C.c_int, vp,
                                          vp, vp]),
             "vpm_plan_download_fluid": (C.c_int, [vp, C.POINTER(VpmFluidOut)]),
-            "vpm_plan_step": (C.c_int, [vp, _D, C.c_double, C.c_int, _D, C.c_double, vp, vp]),
+            "vpm_plan_step": (C.c_int, [vp, vp, C.c_double, C.c_int, vp, C.c_double, vp, vp]),
             "vpm_plan_probe": (C.c_int, [vp, _D, C.c_double, _D]),
             "vpm_stream_sync": (C.c_int, [vp]),
             "vpm_plan_stage_fluid": (C.c_int, [vp, C.POINTER(VpmFluid)]),

@@ -23,7 +23,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from ._lib import _D, check, ptr
+from ._lib import _D, addr, check, ptr
 from .device import DevicePlan
 from .vpm import FluidState
 
@@ -45,6 +45,9 @@ class DeviceWake:
         self._int = raw[96:116].view(np.int32)  # rc n_wake ring_a ring_b n_prev
         self._x = np.zeros(7)
         self._s2 = np.zeros(2)
+        # fixed addresses, looked up once (the per-tick call passes plain integers)
+        self._x_addr, self._s2_addr, self._rec_addr = addr(self._x), addr(self._s2), self._rec.data_ptr()
+        self._stream_addr = self.stream.cuda_stream
         self.n_wake, self.ring_a, self.ring_b = fluid.n_wake, fluid.ring_a, fluid.ring_b
         self.rc = 0
 
@@ -53,7 +56,7 @@ class DeviceWake:
         return None if self.ring_a < 0 else (self.ring_a, self.ring_b)
 
     def _s(self):
-        return C.c_void_p(self.stream.cuda_stream)
+        return C.c_void_p(self._stream_addr)
 
     def step_async(self, x, u: float, integrate: bool, sensor=None, r_core: float = 0.0) -> None:
         """Queue one Engine.step (integrate) / fluid_step on the stream (state and
@@ -64,9 +67,9 @@ class DeviceWake:
         sp = None
         if sensor is not None:
             self._s2[:] = sensor
-            sp = ptr(self._s2, _D)
-        check(_lib.lib().vpm_plan_step(self.plan.handle, ptr(self._x, _D), float(u), int(bool(integrate)), sp,
-                                       float(r_core), C.c_void_p(self._rec.data_ptr()), self._s()), "plan_step")
+            sp = self._s2_addr
+        check(_lib.lib().vpm_plan_step(self.plan.handle, self._x_addr, float(u), int(bool(integrate)), sp,
+                                       float(r_core), self._rec_addr, self._stream_addr), "plan_step")
 
     def sync(self) -> None:
         check(_lib.lib().vpm_stream_sync(self._s()), "stream_sync")
