@@ -267,6 +267,23 @@ def _time_ms(torch, fn, reps=3):
     return best
 
 
+def _b2b_ms(torch, fn, reps=10):
+    """Device time per call of ``reps`` back-to-back calls (CUDA events around the
+    batch; the host enqueues ahead of the GPU, so no launch gap enters), best of 3."""
+    fn()
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b) / reps)
+    return best
+
+
 def extras(torch, dev, sc, flat, plan, mp):
     """Side measurements (not the headline): the C2 latency config, policy
     synthesis on the C4 snapshot, and the C5 Biot-Savart stress sweep."""
@@ -285,9 +302,10 @@ def extras(torch, dev, sc, flat, plan, mp):
            "partial": torch.empty(HORIZON + 2, dtype=torch.float64, device=dev),
            "flag": torch.zeros(1, dtype=torch.int32, device=dev)}
     u2 = f64(np.full(HORIZON, -6.0))
-    x2 = f64(s2["x0"])
-    out["c2_iteration_ms"] = _time_ms(torch, lambda: p2.mppi_iteration(
-        x2, u2, n2, SIGMA, 257, LAMBDA, f64(Q), f64(XPERCH), sc2))
+    x2, q_d, xp_d = f64(s2["x0"]), f64(Q), f64(XPERCH)
+    # device time of one iteration (rollouts + fused softmax update), iterations back to back
+    out["c2_iteration_ms"] = _b2b_ms(torch, lambda: p2.mppi_iteration(
+        x2, u2, n2, SIGMA, 257, LAMBDA, q_d, xp_d, sc2))
     # C3: K=1024 (+1), H=50, N<=256 + ring (reference-generated prefilled wake)
     with np.load(os.path.join(ROOT, "tests", "golden", "scenario_C3.npz")) as z:
         s3 = {k: z[k] for k in z.files}
@@ -299,11 +317,35 @@ def extras(torch, dev, sc, flat, plan, mp):
     sc3 = {"cost": torch.empty(1025, dtype=torch.float64, device=dev),
            "partial": torch.empty(HORIZON + 2, dtype=torch.float64, device=dev),
            "flag": torch.zeros(1, dtype=torch.int32, device=dev)}
-    u3 = f64(np.full(HORIZON, -6.0))
-    ms3 = _time_ms(torch, lambda: p3.mppi_iteration(f64(s3["x0"]), u3, n3, SIGMA, 1025, LAMBDA, f64(Q),
-                                                     f64(XPERCH), sc3))
+    u3, x3 = f64(np.full(HORIZON, -6.0)), f64(s3["x0"])
+    ms3 = _b2b_ms(torch, lambda: p3.mppi_iteration(x3, u3, n3, SIGMA, 1025, LAMBDA, q_d, xp_d, sc3))
     out["c3_iteration"] = {"ms": ms3, "rollouts_per_s": 1025 / (ms3 * 1e-3),
                            "config": "C3: K=1024 (+incumbent), H=50, N<=256 + ring, 1 GPU"}
+    # one rank's share of the C4 iteration at 8 GPUs (rows [0, 513) of 4097): its
+    # rollouts, its softmax partial and the rank-ordered combine (a W = 1 stand-in for
+    # the W = 8 combine; the all-gather of 8 x (H+2) doubles is not on one GPU)
+    from paper_2509_16079_b200.device import mppi_combine
+    from paper_2509_16079_b200.sharding import row_range
+    b8, e8 = row_range(mp.B, 8, 0)
+    o8 = {"status": torch.empty(e8 - b8, dtype=torch.int64, device=dev),
+          "finals": torch.empty(e8 - b8, 7, dtype=torch.float64, device=dev),
+          "cost": torch.empty(e8 - b8, dtype=torch.float64, device=dev)}
+    part8, flag8 = torch.empty(mp.T + 2, dtype=torch.float64, device=dev), torch.zeros(1, dtype=torch.int32,
+                                                                                       device=dev)
+    us8 = mp.ustar.clone()
+    u8 = us8.clone()
+
+    def rank_share():
+        plan.batch(mp.x0, mp.T, ustar=us8, noise=mp.noise, sigma=mp.sigma, row_begin=b8, rows=e8 - b8, q=mp.q,
+                   x_perch=mp.xp, out=o8)
+        plan.mppi_partial(o8["cost"], us8, mp.noise, mp.sigma, mp.temperature, row_begin=b8, partial=part8)
+        mppi_combine(part8.view(1, -1), mp.temperature, u8, flag8)
+
+    ms8 = _b2b_ms(torch, rank_share)
+    out["c4_rank_share_8gpu"] = {"rows": e8 - b8, "ms": ms8, "expected_8gpu_iteration_ms": ms8 + 0.05,
+                                 "note": "rank 0's rows of the C4 batch at world 8 + its partial + combine, "
+                                         "device-timed back to back on one GPU; + <=0.05 ms all-gather "
+                                         "(DESIGN.md 5)"}
     # policy synthesis (64 perturbed rollouts on the N=512 + ring snapshot, regression,
     # Riccati) through the C ABI with host buffers, around the current u*
     cfg = config.ExperimentConfig()

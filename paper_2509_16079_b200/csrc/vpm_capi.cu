@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -771,14 +772,17 @@ int vpm_plan_download_fluid(vpm_plan *p, vpm_fluid_out *out) {
   return VPM_OK;
 }
 
-int vpm_mppi_partial(vpm_plan *p, const double *d_cost, int rows, int row_begin,
-                     const double *d_ustar, const double *d_noise, double sigma, int T,
-                     double temperature, double *d_partial, void *stream) {
+// One launch of the shard's softmax partial (vpm_rollout.cuh, mppi_partial_chunked_kernel);
+// ustar_out / flag: apply the single-device update in the same launch.
+static int partial_launch(vpm_plan *p, const double *d_cost, int rows, int row_begin, const double *d_ustar,
+                          const double *d_noise, double sigma, int T, double temperature, double *d_partial,
+                          double *d_ustar_out, int32_t *d_flag, void *stream) {
   if (!p) return fail_cfg("null plan");
   if (temperature <= 0.0) return fail_cfg("temperature must be > 0");
+  if (rows < 0 || T < 0) return fail_cfg("bad partial shape");
   std::lock_guard<std::mutex> lk(p->mu);
   CK(cudaSetDevice(p->device));
-  const int G = rows > 0 ? (rows + vpm::PCH_ROWS - 1) / vpm::PCH_ROWS : 1;
+  const int G = std::max(1, (rows + vpm::PCH_ROWS - 1) / vpm::PCH_ROWS);
   const size_t need = (size_t)G * (T + 2);
   if (p->wbuf_len < need) {
     cudaFree(p->d_wbuf);
@@ -790,15 +794,23 @@ int vpm_mppi_partial(vpm_plan *p, const double *d_cost, int rows, int row_begin,
     CK(cudaMalloc(&p->d_ticket, sizeof(unsigned)));
     CK(cudaMemset(p->d_ticket, 0, sizeof(unsigned)));
   }
-  const size_t smem = sizeof(double) * ((size_t)vpm::PCH_WARPS * (T + 1) + 3 * vpm::PCH_WARPS);
+  // shared memory: [NW][T+1] sums | 2 NW reductions | T+1 totals
+  const size_t smem = sizeof(double) * ((size_t)vpm::PCH_WARPS * (T + 1) + 2 * vpm::PCH_WARPS + (T + 1));
   if (smem > 48 * 1024)
     CK(cudaFuncSetAttribute(vpm::mppi_partial_chunked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
   vpm::mppi_partial_chunked_kernel<<<G, 32 * vpm::PCH_WARPS, smem, (cudaStream_t)stream>>>(
       d_cost, rows, row_begin, d_ustar, d_noise, sigma, p->P.u_lim, T, temperature, p->d_wbuf, p->d_ticket,
-      d_partial);
+      d_partial, d_ustar_out, d_flag);
   CK(cudaGetLastError());
   return VPM_OK;
+}
+
+int vpm_mppi_partial(vpm_plan *p, const double *d_cost, int rows, int row_begin,
+                     const double *d_ustar, const double *d_noise, double sigma, int T,
+                     double temperature, double *d_partial, void *stream) {
+  return partial_launch(p, d_cost, rows, row_begin, d_ustar, d_noise, sigma, T, temperature, d_partial, nullptr,
+                        nullptr, stream);
 }
 
 int vpm_mppi_combine(const double *d_partials, int W, int T, double temperature, double *d_ustar,
@@ -844,9 +856,9 @@ int vpm_mppi_iteration(vpm_plan *p, const double *d_x0, double *d_ustar, const d
   o.cost = d_cost;
   int rc = vpm_plan_batch(p, d_x0, 0, nullptr, d_ustar, d_noise, sigma, 0, B_total, T, d_q, d_xperch, 0, &o, stream);
   if (rc) return rc;
-  rc = vpm_mppi_partial(p, d_cost, B_total, 0, d_ustar, d_noise, sigma, T, temperature, d_partial, stream);
-  if (rc) return rc;
-  return vpm_mppi_combine(d_partial, 1, T, temperature, d_ustar, d_flag, stream);
+  // partial + the W = 1 combine in one launch (bitwise vpm_mppi_partial + vpm_mppi_combine)
+  return partial_launch(p, d_cost, B_total, 0, d_ustar, d_noise, sigma, T, temperature, d_partial, d_ustar, d_flag,
+                        stream);
 }
 
 int vpm_mppi_optimize_host(vpm_plan *p, const double *x0, double *u_star, const double *noise,

@@ -1394,80 +1394,122 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
 }
 
 // ---- MPPI reductions -----------------------------------------------------------------
-// Chunked softmax partials of one shard (mppi.py:46-59), a streaming kernel: CTA c
-// owns rows [c CH, c CH + CH) -- each warp 8 consecutive rows, whose control rows
-// (clip(u* + sigma noise), coalesced over t) it loads all at once -- and writes the
-// chunk partial {J_min_c, Z_c, S_c[T]} (weights relative to J_min_c).  The last CTA
-// to finish (ticket) combines the chunk partials in chunk order, rescaled to the
-// shard minimum, into part = {J_min, Z, S[T]}, and re-arms the ticket.  Every sum
-// has a fixed order, so the result does not depend on scheduling.
+// Softmax partial of one shard (mppi.py:46-59): part = {J_min, Z, S[T]} with weights
+// exp(-(J - J_min)/lambda) of the shard's rows and S_t their weighted clipped controls
+// clip(u* + sigma noise).  A latency-bound streaming kernel: CTA c owns rows
+// [64 c, 64 c + 64) -- each warp 8 consecutive rows, whose control rows (coalesced over
+// t; rows with zero weight load nothing) it loads all at once -- and writes the chunk
+// partial {J_min_c, Z_c, S_c[T]} relative to its own minimum.  The last CTA to finish
+// (ticket) combines the chunks in a fixed two-level order, rescaled to the shard
+// minimum, and re-arms the ticket (a one-CTA grid writes its record as the partial).
+// Every sum has a fixed order, so the result does not depend on scheduling.  With
+// ustar_out set (the single-device iteration) the finishing CTA also applies the
+// update u* = S/Z, or raises the sticky failure flag when every row failed -- bitwise
+// what mppi_combine_kernel computes from part with W = 1 (its rescaling factor is
+// exp(-0) = 1), one launch fewer.  Measured alternative: one CTA of 32 warps looping
+// over the rows (no ticket) was slower at every size from 257 rows up -- one SM's
+// FP64 pipe then carries every row's exp and division.
 constexpr int PCH_WARPS = 8, PCH_ROWS = 8 * PCH_WARPS;  // 256 threads, 64 rows per CTA
+
+// fixed-order sum of v[w * stride], w = 0..n-1: four interleaved chains, then
+// (c0 + c1) + (c2 + c3) -- a quarter of the dependent shared-load latency
+__device__ __forceinline__ double sum_strided4(const double *v, int n, int stride) {
+  double c[4] = {0.0, 0.0, 0.0, 0.0};
+  int w = 0;
+  for (; w < n; w += 4) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (w + q < n) c[q] += v[(w + q) * stride];
+  }
+  return (c[0] + c[1]) + (c[2] + c[3]);
+}
+
+// lanes' values added by a fixed xor butterfly (every lane gets the same sum)
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+  for (int o = 16; o >= 1; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 __global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
-    const double *__restrict__ cost, int rows, int row_begin, const double *__restrict__ ustar,
+    const double *__restrict__ cost, int rows, int row_begin, const double *ustar,
     const double *__restrict__ noise, double sigma, double ulim, int T, double lambda,
-    double *__restrict__ chunks, unsigned *__restrict__ ticket, double *__restrict__ part) {
-  // [PCH_WARPS][T+1] control sums (then the last CTA's group sums) | 3 PCH_WARPS
-  // reductions
+    double *__restrict__ chunks, unsigned *__restrict__ ticket, double *__restrict__ part, double *ustar_out,
+    int32_t *__restrict__ flag) {
+  // [NW][T+1] control sums (then the last CTA's group sums) | NW + NW reductions |
+  // T+1 totals
   extern __shared__ double sh[];
-  double *sacc = sh, *sred = sh + PCH_WARPS * (T + 1);
+  constexpr int NW = PCH_WARPS;
+  double *sacc = sh, *sred = sh + NW * (T + 1), *stot = sred + 2 * NW;
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ld = T + 2;
   const int rw = blockIdx.x * PCH_ROWS + warp * 8;  // this warp's first row
-  // costs of the warp's 8 rows (lane j < 8 holds row j)
-  const double Jl = (lane < 8 && rw + lane < rows) ? cost[rw + lane] : INFINITY;
-  double jm = isfinite(Jl) ? Jl : INFINITY;
-  for (int o = 4; o >= 1; o >>= 1) jm = fmin(jm, __shfl_xor_sync(0xffffffffu, jm, o));
+  // the CTA's cost minimum (exact, order-free); lane j < 8 holds row j
+  double Jl = (lane < 8 && rw + lane < rows) ? cost[rw + lane] : INFINITY;
+  Jl = isfinite(Jl) ? Jl : INFINITY;
+  double jm = warp_min(Jl);
   if (lane == 0) sred[warp] = jm;
   __syncthreads();
-  jm = INFINITY;
-  for (int w = 0; w < PCH_WARPS; ++w) jm = fmin(jm, sred[w]);  // chunk minimum (exact)
+  jm = warp_min(lane < NW ? sred[lane] : INFINITY);
   const bool any = isfinite(jm);
   const double wl = (any && isfinite(Jl)) ? exp(-(Jl - jm) / lambda) : 0.0;
-  double z = wl;  // lanes >= 8 hold 0; fixed butterfly over the 8 rows
-  for (int o = 4; o >= 1; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-  double wr[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) wr[j] = __shfl_sync(0xffffffffu, wl, j);
+  const double z = warp_sum(wl);  // lanes >= 8 hold 0: fixed butterfly over the 8 rows
+  // bit j: row j carries weight and has a noise row (row 0 of the batch is the
+  // incumbent u* itself)
+  const unsigned live = __ballot_sync(0xffffffffu, wl != 0.0 && row_begin + rw + lane > 0);
   for (int tc = 0; tc < T; tc += 64) {
     const int t0 = tc + lane, t1 = tc + 32 + lane;
     const double us0 = t0 < T ? ustar[t0] : 0.0, us1 = t1 < T ? ustar[t1] : 0.0;
-    double u0[8], u1[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {  // all loads of the 8 rows first
-      const int g = row_begin + rw + j;
-      u0[j] = us0;
-      u1[j] = us1;
-      if (wr[j] != 0.0 && g > 0) {
-        const double *nz = noise + (size_t)(g - 1) * T;
-        if (t0 < T) u0[j] = clampd(us0 + nz[t0] * sigma, -ulim, ulim);
-        if (t1 < T) u1[j] = clampd(us1 + nz[t1] * sigma, -ulim, ulim);
-      }
-    }
     double a0 = 0.0, a1 = 0.0;
+    // all 16 noise loads in flight at once: load-only predicated bodies (a branch
+    // around load + arithmetic made them one round trip per row)
+    double n0[8], n1[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double *nz = noise + (size_t)max(row_begin + rw + j - 1, 0) * T;
+      const bool lj = (live >> j) & 1u;
+      n0[j] = 0.0;
+      n1[j] = 0.0;
+      if (lj && t0 < T) n0[j] = nz[t0];
+      if (lj && t1 < T) n1[j] = nz[t1];
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {  // row order
-      a0 += wr[j] * u0[j];
-      a1 += wr[j] * u1[j];
+      const double w = __shfl_sync(0xffffffffu, wl, j);
+      const bool lj = (live >> j) & 1u;
+      const double u0 = (lj && t0 < T) ? clampd(us0 + n0[j] * sigma, -ulim, ulim) : us0;
+      const double u1 = (lj && t1 < T) ? clampd(us1 + n1[j] * sigma, -ulim, ulim) : us1;
+      a0 += w * u0;
+      a1 += w * u1;
     }
     if (t0 < T) sacc[warp * T + t0] = a0;
     if (t1 < T) sacc[warp * T + t1] = a1;
   }
-  if (lane == 0) sred[PCH_WARPS + warp] = z;
+  if (lane == 0) sred[NW + warp] = z;
   __syncthreads();
-  double *mine = chunks + (size_t)blockIdx.x * ld;
+  // the CTA's record {J_min, Z, S[T]}: warps added in a fixed order
+  const double Z = warp_sum(lane < NW ? sred[NW + lane] : 0.0);
+  const bool solo = gridDim.x == 1;  // one chunk: the record is the shard partial
+  double *mine = solo ? part : chunks + (size_t)blockIdx.x * ld;
   if (threadIdx.x == 0) {
-    double Z = 0.0;
-    for (int w = 0; w < PCH_WARPS; ++w) Z += sred[PCH_WARPS + w];
     mine[0] = jm;
     mine[1] = Z;
   }
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
-    double S = 0.0;
-    for (int w = 0; w < PCH_WARPS; ++w) S += sacc[w * T + t];
+    const double S = sum_strided4(sacc + t, NW, T);
     mine[2 + t] = S;
+    // the W = 1 combine (mppi_combine_kernel): Z = 0 + Z_0 * 1, S_t = 0 + S_t,0 * 1
+    if (solo && ustar_out && any) ustar_out[t] = (0.0 + S) / (0.0 + Z);
   }
-  // last CTA: combine the chunks in chunk order
+  if (solo) {
+    if (ustar_out && !any && threadIdx.x == 0 && flag) *flag = 1;  // sticky failure flag
+    return;
+  }
+  // chunked: the last CTA combines the chunks in chunk order
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
@@ -1479,17 +1521,16 @@ __global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
   // global minimum: all chunk minima loaded in parallel (min is exact, order-free)
   double gm = INFINITY;
   for (int c = threadIdx.x; c < G; c += blockDim.x) gm = fmin(gm, __ldcg(chunks + (size_t)c * ld));
-  for (int o = 16; o >= 1; o >>= 1) gm = fmin(gm, __shfl_xor_sync(0xffffffffu, gm, o));
-  if (lane == 0) sred[2 * PCH_WARPS + warp] = gm;
+  gm = warp_min(gm);
+  if (lane == 0) sred[warp] = gm;
   __syncthreads();
-  gm = INFINITY;
-  for (int w = 0; w < PCH_WARPS; ++w) gm = fmin(gm, sred[2 * PCH_WARPS + w]);
+  gm = warp_min(lane < NW ? sred[lane] : INFINITY);
   // Z and S in a fixed two-level order: warp w sums the contiguous chunk group
-  // [w G / PCH_WARPS, (w+1) G / PCH_WARPS) in chunk order (lanes over the T+1
-  // columns {Z, S_0..S_T-1}, coalesced chunk-row loads), then the group sums are
-  // added in group order.  The order depends only on G.
-  double *gsum = sacc;  // [PCH_WARPS][T+1], the chunk's control sums are no longer needed
-  const int c_lo = (int)((long long)warp * G / PCH_WARPS), c_hi = (int)((long long)(warp + 1) * G / PCH_WARPS);
+  // [w G / NW, (w+1) G / NW) in chunk order (lanes over the T+1 columns
+  // {Z, S_0..S_T-1}, coalesced chunk-row loads), then the group sums are added in
+  // group order.  The order depends only on G.
+  double *gsum = sacc;  // [NW][T+1], the chunk's control sums are no longer needed
+  const int c_lo = (int)((long long)warp * G / NW), c_hi = (int)((long long)(warp + 1) * G / NW);
   for (int col0 = 0; col0 < T + 1; col0 += 32) {
     const int col = col0 + lane;
     double acc = 0.0;
@@ -1518,12 +1559,21 @@ __global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
   __syncthreads();
   for (int col = threadIdx.x; col < T + 1; col += blockDim.x) {
     double tot = 0.0;
-    for (int w = 0; w < PCH_WARPS; ++w) tot += gsum[w * (T + 1) + col];
+    for (int w = 0; w < NW; ++w) tot += gsum[w * (T + 1) + col];
     part[1 + col] = tot;  // part[1] = Z, part[2 + t] = S_t
+    stot[col] = tot;
   }
   if (threadIdx.x == 0) {
     part[0] = gm;
     *ticket = 0u;
+  }
+  if (ustar_out) {  // the W = 1 combine, from the totals on chip
+    __syncthreads();
+    if (!isfinite(gm)) {
+      if (threadIdx.x == 0 && flag) *flag = 1;
+    } else {
+      for (int t = threadIdx.x; t < T; t += blockDim.x) ustar_out[t] = (0.0 + stot[1 + t]) / (0.0 + stot[0]);
+    }
   }
 }
 

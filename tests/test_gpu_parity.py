@@ -329,6 +329,46 @@ def test_mppi_update_vs_oracle(torch_cuda, oracle_core):
     assert_close(new.cpu().numpy(), u_ref, "u", what="u*")
 
 
+@pytest.mark.parametrize("K,x0_mode", [(40, "scenario"), (128, "scenario"), (1024, "scenario"),
+                                         (128, "blowup")])
+def test_fused_iteration_equals_partial_plus_combine(torch_cuda, K, x0_mode):
+    """vpm_mppi_iteration applies the W = 1 combine inside the softmax partial's
+    finishing CTA: u*, the partial record and the sticky failure flag are bitwise what
+    batch + vpm_mppi_partial + vpm_mppi_combine give -- for one chunk (K+1 <= 64),
+    several chunks (last-CTA combine) and a batch whose every rollout fails (u* kept,
+    flag raised)."""
+    import torch
+    from paper_2509_16079_b200.device import DevicePlan, mppi_combine
+    sc = golden("scenario_C3.npz")
+    plan = DevicePlan(sc["iparams"], sc["fparams"])
+    plan.set_fluid(flat_of(sc))
+    dev = torch.device("cuda")
+    f64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev)
+    x0 = f64(sc["x0"] if x0_mode == "scenario" else [0.0, 0.0, 0.0, 0.0, 7.0, 0.0, 299.9])
+    q, xp = f64([10, 10, 1, 0, 0.2, 0.2, 0.2]), f64([3.5, 0, np.pi / 4, 0, 0.5, -0.5, 0])
+    noise = f64(np.random.default_rng(K).normal(0.0, 1.0, (K, 50)))
+    us = f64(sc["warm"])
+    scratch = {"cost": torch.empty(K + 1, dtype=torch.float64, device=dev),
+               "partial": torch.empty(52, dtype=torch.float64, device=dev),
+               "flag": torch.zeros(1, dtype=torch.int32, device=dev)}
+    u_fused = us.clone()
+    plan.mppi_iteration(x0, u_fused, noise, 2.0, K + 1, 0.05, q, xp, scratch)
+    out = plan.batch(x0, 50, ustar=us, noise=noise, sigma=2.0, rows=K + 1, q=q, x_perch=xp)
+    part = plan.mppi_partial(out["cost"], us, noise, 2.0, 0.05)
+    u_sep, flag = us.clone(), torch.zeros(1, dtype=torch.int32, device=dev)
+    mppi_combine(part.view(1, -1), 0.05, u_sep, flag)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(scratch["cost"].cpu().numpy(), out["cost"].cpu().numpy())
+    np.testing.assert_array_equal(scratch["partial"].cpu().numpy(), part.cpu().numpy())
+    np.testing.assert_array_equal(u_fused.cpu().numpy(), u_sep.cpu().numpy())
+    assert int(scratch["flag"].item()) == int(flag.item()) == (1 if x0_mode == "blowup" else 0)
+    if x0_mode == "blowup":
+        assert not np.isfinite(out["cost"].cpu().numpy()).any()
+        np.testing.assert_array_equal(u_fused.cpu().numpy(), sc["warm"])  # u* left unchanged
+    else:
+        assert not np.array_equal(u_fused.cpu().numpy(), sc["warm"])
+
+
 def test_policy_C2_golden(torch_cuda):
     from paper_2509_16079_b200 import config, policy
     g = golden("policy_C2.npz")
