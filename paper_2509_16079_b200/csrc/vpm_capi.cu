@@ -214,10 +214,12 @@ Shape pick_shape(int cap, int nb, int rows) {
         c = std::min(c, (int)((228 * 1024) / smem));
         return (c < 1 || (regs > 64 && c * s.nt < 768)) ? 1 << 30 : ((n_sm + c - 1) / c) * c;
       };
+      // fewest slots; ties to the smaller register budget (more resident warps:
+      // C5 N = 512, 112 slots either way, 64 registers 1% faster than 72)
       int bs = slots(64);
       for (int regs : {72, 80}) {
         const int sl = slots(regs);
-        if (sl <= bs) {
+        if (sl < bs) {
           bs = sl;
           s.minb = regs;
         }
@@ -254,14 +256,12 @@ Shape pick_shape(int cap, int nb, int rows) {
   // Wave quantisation: with c CTAs resident per SM (register-limited) a
   // throughput-bound launch costs ~ceil(n/c) * c rollout-slots per SM, whatever c
   // is.  Among the 64 / 72 / 80-register variants take the fewest slots, ties to
-  // the larger register budget (the sweep interleaves more chains).  4097 rows on
-  // 148 SMs (28 per SM): 128 threads at 72 registers = 4 x 7 = 28 slots instead of
-  // 4 x 8 = 32; C5 (16384 rows, 111 per SM) at N = 512: 112 slots either way, 72
-  // registers 3.5% faster; at N = 1024 (256 threads) 72 registers (3 CTAs/SM) 1.5%
-  // faster than 64 (4 CTAs/SM).  Variants that leave fewer than 3 CTAs per SM are
-  // excluded (N = 2048, 512 threads: 1 CTA/SM at 72 registers is 8% slower than 2
-  // at 64), and 64-thread CTAs keep 64 (N = 256: 72 registers 2% slower at equal
-  // slots).  Latency-bound launches (one round) keep 64.
+  // the larger register budget (the direct sweep interleaves more chains; measured
+  // in round 1 with the direct sweep at caps 512 / 1024, which now take the
+  // symmetric sweep and its own rule above: 72 registers 3.5% / 1.5% faster at equal
+  // or fewer slots).  Variants that leave fewer than 3 CTAs per SM are excluded, and
+  // 64-thread CTAs keep 64 (N = 256: 72 registers 2% slower at equal slots).
+  // Latency-bound launches (one round) keep 64.
   const int n_sm = (int)ceil(per_sm);
   if (per_sm > 8.0 && best.nt >= 128) {
     const size_t smem = vpm::make_layout(cap, nb, best.nt).total + 1024;
@@ -1263,7 +1263,7 @@ int vpm_policy_fit(const double *d_nom_x, const double *d_nom_u, const double *d
     CK(cudaGetLastError());
   }
   if (do_riccati) {
-    vpm::riccati_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(a);
+    vpm::riccati_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(a);
     CK(cudaGetLastError());
   }
   return VPM_OK;

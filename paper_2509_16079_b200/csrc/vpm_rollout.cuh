@@ -1674,7 +1674,7 @@ __device__ __forceinline__ void cloud_row(const PolicyArgs &p, int i, int k, con
 // (assemble_discrete, policy.py:121-138).
 // The steps are independent: they are spread over the whole GPU (PFIT_WARPS warps
 // per CTA, ceil(H / PFIT_WARPS) CTAs) -- one CTA of 16 warps took 5 rounds on one SM.
-// Phase 2 (riccati_kernel, one warp, launched after): backward Riccati recursion
+// Phase 2 (riccati_kernel, one 64-thread CTA, launched after): backward Riccati recursion
 // S_N = Q_f, h_k = (b'S A)/(r + b'S b), S <- Q + A'S A - (A'S b) h', symmetrised
 // (tvlqr_backward, policy.py:206-233).
 constexpr int PFIT_WARPS = 2;
@@ -1784,78 +1784,58 @@ __global__ void __launch_bounds__(32 * PFIT_WARPS) policy_fit_kernel(const Polic
   }
 }
 
-__global__ void __launch_bounds__(32) riccati_kernel(const PolicyArgs p) {
-  __shared__ double S[49], SA[49], A[49], Sn[49], bv[7], Sb[7], bS[7], AtSb[7], hh[7];
-  const int lane = threadIdx.x & 31;
-  for (int e = lane; e < 49; e += 32) S[e] = (e % 8 == 0) ? p.qf[e / 7] : 0.0;
-  if (lane == 0) p.flag[0] = 0;
+// One thread per entry of the 7x7 recursion (64 threads, 3 barriers per step).  S is
+// kept exactly symmetric (the symmetrisation adds the same two numbers either way
+// round), so b'S = (S b)' and one product serves both; every dot product runs over its
+// index in order, as the one-warp form it replaces did (bitwise the same gains).
+__device__ __forceinline__ double dot7(const double *x, int sx, const double *y, int sy) {
+  double v = 0.0;
+#pragma unroll
+  for (int m = 0; m < 7; ++m) v += x[m * sx] * y[m * sy];
+  return v;
+}
+
+__global__ void __launch_bounds__(64) riccati_kernel(const PolicyArgs p) {
+  __shared__ double S[49], SA[49], A[49], Sn[49], bv[7], Sb[7];
+  const int tid = threadIdx.x;
+  const bool ent = tid < 49;  // thread e < 49 owns entry (i, j) = (e / 7, e % 7)
+  const int i = ent ? tid / 7 : 0, j = ent ? tid % 7 : 0;
+  if (ent) S[tid] = i == j ? p.qf[i] : 0.0;
+  const double qd = (ent && i == j) ? p.qr[i] : 0.0;  // running-cost diagonal entry
+  if (tid == 0) p.flag[0] = 0;
   // (A_k, b_k) of the next step are loaded into registers while step k+1 computes:
   // the recursion is serial, so an L2 round trip per step would sit on its path
-  double a0 = 0.0, a1 = 0.0, b0 = 0.0;
-  {
-    const int k = p.H - 1;
-    a0 = p.a_disc[(size_t)k * 49 + lane];
-    if (lane + 32 < 49) a1 = p.a_disc[(size_t)k * 49 + lane + 32];
-    if (lane < 7) b0 = p.b_disc[(size_t)k * 7 + lane];
-  }
-  __syncwarp();
+  double an = 0.0, bn = 0.0;
+  if (ent) an = p.a_disc[(size_t)(p.H - 1) * 49 + tid];
+  if (tid < 7) bn = p.b_disc[(size_t)(p.H - 1) * 7 + tid];
   for (int k = p.H - 1; k >= 0; --k) {
-    A[lane] = a0;
-    if (lane + 32 < 49) A[lane + 32] = a1;
-    if (lane < 7) bv[lane] = b0;
+    if (ent) A[tid] = an;
+    if (tid < 7) bv[tid] = bn;
     if (k > 0) {
-      a0 = p.a_disc[(size_t)(k - 1) * 49 + lane];
-      if (lane + 32 < 49) a1 = p.a_disc[(size_t)(k - 1) * 49 + lane + 32];
-      if (lane < 7) b0 = p.b_disc[(size_t)(k - 1) * 7 + lane];
+      if (ent) an = p.a_disc[(size_t)(k - 1) * 49 + tid];
+      if (tid < 7) bn = p.b_disc[(size_t)(k - 1) * 7 + tid];
     }
-    __syncwarp();
-    if (lane < 7) {
-      double s1 = 0.0, s2 = 0.0;
-      for (int j = 0; j < 7; ++j) {
-        s1 += S[lane * 7 + j] * bv[j];  // (S b)_i
-        s2 += bv[j] * S[j * 7 + lane];  // (b' S)_j
-      }
-      Sb[lane] = s1;
-      bS[lane] = s2;
+    __syncthreads();  // A_k, b_k and S_{k+1} visible
+    if (ent) SA[tid] = dot7(S + 7 * i, 1, A + j, 7);                              // (S A)_ij
+    else if (tid < 56) Sb[tid - 49] = dot7(S + 7 * (tid - 49), 1, bv, 1);        // (S b)_i
+    __syncthreads();
+    if (ent) {
+      double denom = p.r;
+      for (int m = 0; m < 7; ++m) denom += bv[m] * Sb[m];
+      const double gj = dot7(A + j, 7, Sb, 1), gi = dot7(A + i, 7, Sb, 1);  // (A' S b)_j, _i
+      const double hj = gj / denom;
+      if (i == 0) p.gains[(size_t)k * 7 + j] = hj;
+      Sn[tid] = qd + dot7(A + i, 7, SA + j, 7) - gi * hj;
     }
-    for (int e = lane; e < 49; e += 32) {
-      const int i = e / 7, j = e % 7;
-      double v = 0.0;
-      for (int m = 0; m < 7; ++m) v += S[i * 7 + m] * A[m * 7 + j];
-      SA[e] = v;
-    }
-    __syncwarp();
-    double denom = p.r;
-    for (int i = 0; i < 7; ++i) denom += bv[i] * Sb[i];
-    if (lane < 7) {
-      double v = 0.0, w = 0.0;
-      for (int i = 0; i < 7; ++i) {
-        v += bS[i] * A[i * 7 + lane];
-        w += A[i * 7 + lane] * Sb[i];
-      }
-      hh[lane] = v / denom;
-      AtSb[lane] = w;
-      p.gains[(size_t)k * 7 + lane] = v / denom;
-    }
-    __syncwarp();
-    for (int e = lane; e < 49; e += 32) {
-      const int i = e / 7, j = e % 7;
-      double v = 0.0;
-      for (int m = 0; m < 7; ++m) v += A[m * 7 + i] * SA[m * 7 + j];
-      Sn[e] = (i == j ? p.qr[i] : 0.0) + v - AtSb[i] * hh[j];
-    }
-    __syncwarp();
+    __syncthreads();
     bool fin = true;
-    for (int e = lane; e < 49; e += 32) {
-      const int i = e / 7, j = e % 7;
-      const double v = 0.5 * (Sn[i * 7 + j] + Sn[j * 7 + i]);
-      S[e] = v;
-      fin = fin && isfinite(v);
+    if (ent) {
+      const double v = 0.5 * (Sn[tid] + Sn[7 * j + i]);
+      S[tid] = v;
+      fin = isfinite(v);
     }
-    fin = __all_sync(0xffffffffu, fin);
-    __syncwarp();
-    if (!fin) {
-      if (lane == 0) p.flag[0] = 1 + k;
+    if (!__syncthreads_and(fin)) {
+      if (tid == 0) p.flag[0] = 1 + k;
       return;
     }
   }
