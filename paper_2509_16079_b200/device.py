@@ -260,8 +260,12 @@ def policy_fit(nom_x, nom_u, cloud_x, cloud_u, status, dt: float, q_running, r_r
     torch = _torch()
     H, K = int(nom_u.shape[0]), int(cloud_u.shape[0])
     dev = nom_x.device
-    z = lambda *s: torch.zeros(*s, dtype=torch.float64, device=dev)
-    ac, bc, ad, bd, g = z(H, 3, 5), z(H, 3), z(H, 7, 7), z(H, 7), z(H, 7)
+    # one uninitialised block, no fill kernels: the fit writes every entry of (ac, bc,
+    # ad, bd) for every step, the Riccati every gain (on divergence it raises the flag
+    # and the gains are not used); the flag itself must start at 0
+    blk = torch.empty(H * (15 + 3 + 49 + 7 + 7), dtype=torch.float64, device=dev)
+    ac, bc, ad, bd, g = (v.view(H, *sh) for v, sh in zip(
+        torch.split(blk, [H * 15, H * 3, H * 49, H * 7, H * 7]), ((3, 5), (3,), (7, 7), (7,), (7,))))
     flag = torch.zeros(4, dtype=torch.int32, device=dev)
     with _on(nom_x):
         _policy_fit_call(nom_x, nom_u, cloud_x, cloud_u, status, K, H, dt, q_running, r_running, q_final,
