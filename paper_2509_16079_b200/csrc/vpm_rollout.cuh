@@ -591,10 +591,24 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 }
 
 // raw slot of the c-th live particle, skipping the sorted hole list
+// ROLLED: keep the hole loop rolled (a few instructions instead of the unrolled copy).
+// The small-tile kernels (R < 4) use it in the epilogue: with many short rollouts per
+// SM (C5 N = 128: 16 CTAs per SM, 5 steps) they are instruction-fetch bound (ncu:
+// no_instruction 26% of the stall samples) and the prologue / epilogue are a large
+// part of every CTA's instruction stream -- C5 N = 128 -6.5%, C3 -0.8%.  In the
+// large kernels the same edit shifted C4 by +0.7% (code layout), so they keep the
+// unrolled form.
+template <bool ROLLED = false>
 __device__ __forceinline__ int raw_index(int c, const int *holes, int nh) {
   int r = c;
-  for (int h = 0; h < nh; ++h)
-    if (holes[h] <= r) ++r;
+  if constexpr (ROLLED) {
+#pragma unroll 1
+    for (int h = 0; h < nh; ++h)
+      if (holes[h] <= r) ++r;
+  } else {
+    for (int h = 0; h < nh; ++h)
+      if (holes[h] <= r) ++r;
+  }
   return r;
 }
 
@@ -1329,7 +1343,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
     const int nl = ctl->n_live, nh = ctl->n_holes;
     const float4 *wfin = wbuf + ctl->cur * L.capbuf;
     unsigned long long hs = 0ull;
-    for (int c = tid; c < nl; c += NT) hs += wake_sig_elem(c, __float_as_int(wfin[raw_index(c, ctl->holes, nh)].w));
+    for (int c = tid; c < nl; c += NT) hs += wake_sig_elem(c, __float_as_int(wfin[raw_index<(R < 4)>(c, ctl->holes, nh)].w));
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
     if (lane == 0) atomicAdd(&ctl->hsum, hs);
@@ -1358,7 +1372,7 @@ __global__ void __maxnreg__(MAXREG) rollout_kernel(const Args a) {
     const float4 *wfin = wbuf + ctl->cur * L.capbuf;
     for (int c = tid; c < cap4; c += NT) {
       if (c < nl) {
-        const float4 v = wfin[raw_index(c, ctl->holes, nh)];
+        const float4 v = wfin[raw_index<(R < 4)>(c, ctl->holes, nh)];
         a.o_wpos[2 * c] = v.x;
         a.o_wpos[2 * c + 1] = v.y;
         a.o_wgam[c] = (double)v.z * TWO_PI;
