@@ -259,11 +259,11 @@ Shape pick_shape(int cap, int nb, int rows) {
   // the larger register budget (the direct sweep interleaves more chains; measured
   // in round 1 with the direct sweep at caps 512 / 1024, which now take the
   // symmetric sweep and its own rule above: 72 registers 3.5% / 1.5% faster at equal
-  // or fewer slots).  Variants that leave fewer than 3 CTAs per SM are excluded, and
-  // 64-thread CTAs keep 64 (N = 256: 72 registers 2% slower at equal slots).
-  // Latency-bound launches (one round) keep 64.
+  // or fewer slots; 64-thread CTAs, end of round 2: C5 N = 128 / 256 at 72 registers
+  // 2% / 1.3% faster than 64 at equal slots).  Variants that leave fewer than 3 CTAs
+  // per SM are excluded.  Latency-bound launches (one round) keep 64.
   const int n_sm = (int)ceil(per_sm);
-  if (per_sm > 8.0 && best.nt >= 128) {
+  if (per_sm > 8.0) {
     const size_t smem = vpm::make_layout(cap, nb, best.nt).total + 1024;
     auto slots = [&](int regs, int min_c) {
       int c = 65536 / (best.nt * regs);
