@@ -236,10 +236,13 @@ int vpm_noise_philox(uint64_t seed, uint64_t iteration, int row_begin, int rows,
 int vpm_noise_philox_dev(const uint64_t *d_seed_iter, uint64_t offset, int row_begin, int rows, int T,
                          double *d_out, void *stream);
 
-/* Whole MPPI iteration on one device (batch + partial + combine): three kernel
- * launches on stream.  use_graph is reserved and ignored (callers that want graph
+/* Whole MPPI iteration on one device (batch + partial + combine): two kernel
+ * launches on stream -- the rollouts, then the softmax partial whose finishing CTA
+ * also applies the W = 1 combine (bitwise vpm_mppi_partial + vpm_mppi_combine; the
+ * same sticky *d_flag).  use_graph is reserved and ignored (callers that want graph
  * replay capture the stream themselves, as replan.py does).
- * d_noise: (B_total - 1, T).  d_cost scratch (B_total) and d_partial (T+2). */
+ * d_noise: (B_total - 1, T).  d_cost scratch (B_total) and d_partial (T+2), which
+ * holds the partial record afterwards. */
 int vpm_mppi_iteration(vpm_plan *p, const double *d_x0, double *d_ustar, const double *d_noise,
                        double sigma, int B_total, int T, double temperature, const double *d_q,
                        const double *d_xperch, double *d_cost, double *d_partial,
