@@ -1438,11 +1438,7 @@ __device__ __forceinline__ double sum_strided4(const double *v, int n, int strid
   return (c[0] + c[1]) + (c[2] + c[3]);
 }
 
-// lanes' values added by a fixed xor butterfly (every lane gets the same sum)
-__device__ __forceinline__ double warp_sum(double v) {
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+// lanes' minimum by an xor butterfly (every lane gets it; min is order-free)
 __device__ __forceinline__ double warp_min(double v) {
   for (int o = 16; o >= 1; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
@@ -1471,7 +1467,7 @@ __global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
   jm = warp_min(lane < NW ? sred[lane] : INFINITY);
   const bool any = isfinite(jm);
   const double wl = (any && isfinite(Jl)) ? exp(-(Jl - jm) / lambda) : 0.0;
-  const double z = warp_sum(wl);  // lanes >= 8 hold 0: fixed butterfly over the 8 rows
+  const double z = warp_sum_d(wl);  // lanes >= 8 hold 0: fixed butterfly over the 8 rows
   // bit j: row j carries weight and has a noise row (row 0 of the batch is the
   // incumbent u* itself)
   const unsigned live = __ballot_sync(0xffffffffu, wl != 0.0 && row_begin + rw + lane > 0);
@@ -1506,7 +1502,7 @@ __global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
   if (lane == 0) sred[NW + warp] = z;
   __syncthreads();
   // the CTA's record {J_min, Z, S[T]}: warps added in a fixed order
-  const double Z = warp_sum(lane < NW ? sred[NW + lane] : 0.0);
+  const double Z = warp_sum_d(lane < NW ? sred[NW + lane] : 0.0);
   const bool solo = gridDim.x == 1;  // one chunk: the record is the shard partial
   double *mine = solo ? part : chunks + (size_t)blockIdx.x * ld;
   if (threadIdx.x == 0) {
