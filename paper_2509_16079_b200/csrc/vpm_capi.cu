@@ -317,10 +317,11 @@ cudaError_t launch_rollouts(Args a, int grid, cudaStream_t st) {
   a.sym = sh.sym;
   const size_t smem = vpm::make_layout(a.P.cap, a.P.nb, sh.nt, sh.sym != 0).total;
 #ifdef VPM_TUNING_SUBSET
-  // tuning builds (tools/): only the shapes the C4 / 8-GPU-shard / C2 launches pick
+  // tuning builds (tools/): only the shapes the C4 / 8-GPU-shard / C2 / C3 / C5 N=128 launches pick
   if (sh.r == 5 && sh.minb == 72) return launch_t<5, 72>(a, grid, sh.nt, smem, st);
   if (sh.r == 5 && sh.minb == 64) return launch_t<5, 64>(a, grid, sh.nt, smem, st);
   if (sh.r == 3 && sh.minb == 64) return launch_t<3, 64>(a, grid, sh.nt, smem, st);
+  if (sh.r == 3 && sh.minb == 72) return launch_t<3, 72>(a, grid, sh.nt, smem, st);
   if (sh.r == 1 && sh.minb == 64) return launch_t<1, 64>(a, grid, sh.nt, smem, st);
   return cudaErrorNotSupported;
 #else
