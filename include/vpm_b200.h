@@ -179,8 +179,9 @@ int vpm_plan_project_dev(vpm_plan *p, const double *d_x0, int T, const double *d
  * PLACE -- the stepped fluid becomes the snapshot, no host round trip of the wake.
  * x (7, host) and u are passed by value; with sensor (host xz) the FP64 induced
  * velocity there (vpm.py:93-128, regularised, r_core) is evaluated on the stepped
- * wake (the NMPC pressure sensor, nmpc.py:73-85).  Queues the launch(es) and ONE
- * copy of the step record into h_record (pinned host, VPM_STEP_RECORD_BYTES):
+ * wake (the NMPC pressure sensor, nmpc.py:73-85).  Queues the launch(es); the step
+ * record lands in h_record (host, VPM_STEP_RECORD_BYTES) -- written by the kernels
+ * directly when h_record is page-locked (pinned), else through one queued copy:
  *   double x[7] (new state), fw[3] {fw_x, fw_z, m_w}, q[2] (sensor velocity);
  *   int32 rc (0 ok, 2 non-finite), n_wake, ring_a, ring_b, n_prev.
  * Returns without synchronising (vpm_stream_sync).  The plant / observed-wake loop
