@@ -1110,8 +1110,9 @@ struct Carve {
 // Shared driver for step / rollout / batch_rollout with host buffers.  Everything is
 // queued on the thread's own stream (the snapshot upload too: the thread-local plan
 // is used on that stream only), the small outputs -- status, rc, finals, loads and
-// the returned fluid -- are carved contiguously on the device and come back in ONE
-// copy through pinned staging; the stream is synchronised once.
+// the returned fluid -- are carved contiguously (one rollout: in the pinned staging,
+// written by the kernel in place; batches: on the device, ONE copy back through the
+// pinned staging); the stream is synchronised once.
 int host_run(const double *x0, int x0_stride, const double *controls, int B, int T,
              const vpm_fluid *fluid, const int64_t *ip, const double *fp, int integrate,
              int check_env, int record, int64_t *status, double *finals, double *trajs,
@@ -1137,8 +1138,25 @@ int host_run(const double *x0, int x0_stride, const double *controls, int B, int
                       sizeof(int64_t) * ((size_t)B + cap4) + sizeof(int32_t) * ((size_t)B + 4);
   void *sc = host_scratch(need);
   if (!sc) return fail_cfg("device scratch allocation failed");
-  Carve cv{(char *)sc};
-  // packed small outputs first (one D2H), then the trajectories, then the inputs
+  // One rollout (Engine.step / fluid_step / rollout): the small outputs live in the
+  // pinned staging itself -- the kernel writes them there through its device alias
+  // (no copy back) -- and so do the inputs (read in place for a single step, else
+  // one pinned upload).  Batches: outputs packed on the device, ONE copy back.
+  char *pin = nullptr, *pin_dev = nullptr;
+  if (B == 1) {
+    pin = host_pinned(need);
+    void *alias = nullptr;
+    if (pin && cudaHostGetDevicePointer(&alias, pin, 0) == cudaSuccess) {
+      pin_dev = (char *)alias;
+    } else {
+      cudaGetLastError();
+      pin = nullptr;
+    }
+  }
+  const bool direct = pin_dev != nullptr;
+  Carve cv{direct ? pin_dev : (char *)sc};
+  Carve cd{(char *)sc};  // device-only buffers
+  // packed small outputs first, then the trajectories, then the inputs
   int64_t *d_st = cv.take<int64_t>(B);
   int32_t *d_rc = cv.take<int32_t>(B);
   double *d_fin = cv.take<double>((size_t)B * 7);
@@ -1156,11 +1174,33 @@ int host_run(const double *x0, int x0_stride, const double *controls, int B, int
     a.o_ema = cv.take<double>(nb);
   }
   const size_t small_bytes = cv.off;
-  double *d_traj = record ? cv.take<double>(ntraj) : nullptr;
-  double *d_x0 = cv.take<double>((size_t)(x0_stride ? B : 1) * 7);
-  double *d_ctrl = cv.take<double>((size_t)B * (T > 0 ? T : 1));
-  char *pin = host_pinned(small_bytes);
-  if (!pin) return fail_cfg("pinned staging allocation failed");
+  if (!direct) cd.off = small_bytes;
+  double *d_traj = record ? cd.take<double>(ntraj) : nullptr;
+  const size_t nx0 = (size_t)(x0_stride ? B : 1) * 7, nctl = (size_t)B * (T > 0 ? T : 1);
+  double *d_x0, *d_ctrl;
+  if (direct && T <= 1) {  // a single step reads its state and control in place
+    d_x0 = cv.take<double>(nx0 + nctl);
+    d_ctrl = d_x0 + nx0;
+    std::memcpy(pin + ((char *)d_x0 - pin_dev), x0, sizeof(double) * nx0);
+    if (T > 0) std::memcpy(pin + ((char *)d_ctrl - pin_dev), controls, sizeof(double) * nctl);
+  } else {
+    d_x0 = cd.take<double>(nx0 + nctl);
+    d_ctrl = d_x0 + nx0;
+    if (direct) {  // one pinned upload of [x0 | controls]
+      double *h_in = cv.take<double>(nx0 + nctl);
+      double *hp = (double *)(pin + ((char *)h_in - pin_dev));
+      std::memcpy(hp, x0, sizeof(double) * nx0);
+      if (T > 0) std::memcpy(hp + nx0, controls, sizeof(double) * nctl);
+      CK(cudaMemcpyAsync(d_x0, hp, sizeof(double) * (nx0 + (T > 0 ? nctl : 0)), cudaMemcpyHostToDevice, st));
+    } else {
+      CK(cudaMemcpyAsync(d_x0, x0, sizeof(double) * nx0, cudaMemcpyHostToDevice, st));
+      if (T > 0) CK(cudaMemcpyAsync(d_ctrl, controls, sizeof(double) * nctl, cudaMemcpyHostToDevice, st));
+    }
+  }
+  if (!direct) {
+    pin = host_pinned(small_bytes);
+    if (!pin) return fail_cfg("pinned staging allocation failed");
+  }
   a.x0 = d_x0;
   a.x0_stride = x0_stride;
   a.controls = d_ctrl;
@@ -1174,15 +1214,14 @@ int host_run(const double *x0, int x0_stride, const double *controls, int B, int
   a.trajs = d_traj;
   a.rc_out = d_rc;
   a.fw_out = d_fw;
-  CK(cudaMemcpyAsync(d_x0, x0, sizeof(double) * (x0_stride ? B : 1) * 7, cudaMemcpyHostToDevice, st));
-  if (T > 0) CK(cudaMemcpyAsync(d_ctrl, controls, sizeof(double) * (size_t)B * T, cudaMemcpyHostToDevice, st));
   if (record) CK(cudaMemsetAsync(d_traj, 0, sizeof(double) * ntraj, st));
   rc = plan_launch(p, a, B, st);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(pin, sc, small_bytes, cudaMemcpyDeviceToHost, st));
+  if (!direct) CK(cudaMemcpyAsync(pin, sc, small_bytes, cudaMemcpyDeviceToHost, st));
   if (trajs && record) CK(cudaMemcpyAsync(trajs, d_traj, sizeof(double) * ntraj, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  auto from = [&](const void *d) { return pin + ((const char *)d - (const char *)sc); };
+  const char *obase = direct ? pin_dev : (const char *)sc;
+  auto from = [&](const void *d) { return pin + ((const char *)d - obase); };
   if (status) std::memcpy(status, from(d_st), sizeof(int64_t) * B);
   if (rc_out) std::memcpy(rc_out, from(d_rc), sizeof(int32_t) * B);
   if (finals) std::memcpy(finals, from(d_fin), sizeof(double) * B * 7);

@@ -1,6 +1,6 @@
 """Single-instance stepping latency split (tuning tool): host wall time per resident
-DeviceWake step (launch + record copy + sync) next to the step kernel's device time
-(CUDA events around 200 queued steps without syncs)."""
+DeviceWake step (launch + sync) next to the step's device time (CUDA events around 200
+queued steps without syncs), and Engine.step with host buffers."""
 import os
 import sys
 import time
@@ -45,5 +45,9 @@ for cap in (60, 512):
         e1.record(s)
     dw.sync()
     dev = 1e3 * e0.elapsed_time(e1) / n
-    print(f"cap {cap} (n_wake {dw.record()[0] if False else dw.n_wake}): wall per synced step {wall:.1f} us, "
-          f"host enqueue {host:.1f} us, device per queued step {dev:.1f} us")
+    t0 = time.perf_counter()
+    for _ in range(n):
+        eng.step(x0, -6.0, fl)
+    es = 1e6 * (time.perf_counter() - t0) / n
+    print(f"cap {cap}: resident step {wall:.1f} us wall (host enqueue {host:.1f} us, device per queued "
+          f"step {dev:.1f} us); Engine.step with host buffers {es:.1f} us")
