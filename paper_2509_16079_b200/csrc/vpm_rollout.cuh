@@ -1545,15 +1545,15 @@ __global__ void __launch_bounds__(32 * PCH_WARPS) mppi_partial_chunked_kernel(
     const int col = col0 + lane;
     double acc = 0.0;
     int c = c_lo;
-    for (; c + 4 <= c_hi; c += 4) {  // four chunk rows in flight per lane
-      double v[4], jc[4];
+    for (; c + 8 <= c_hi; c += 8) {  // eight chunk rows in flight per lane (same order)
+      double v[8], jc[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 8; ++q) {
         jc[q] = __ldcg(chunks + (size_t)(c + q) * ld);
         v[q] = col <= T ? __ldcg(chunks + (size_t)(c + q) * ld + 1 + col) : 0.0;
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 8; ++q) {
         const double sc = (isfinite(gm) && isfinite(jc[q])) ? exp(-(jc[q] - gm) / lambda) : 0.0;
         acc += v[q] * sc;
       }
