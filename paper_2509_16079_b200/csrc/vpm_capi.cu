@@ -367,8 +367,7 @@ struct vpm_plan {
   double *d_wbuf = nullptr;  // chunk partials of the MPPI softmax reduction
   size_t wbuf_len = 0;
   unsigned *d_ticket = nullptr;  // last-CTA ticket of the chunked reduction (re-armed by it)
-  void *d_rec = nullptr;                         // single-step record (vpm_plan_step)
-  void *rec_host = nullptr, *rec_dev = nullptr;  // last caller record buffer and its device alias
+  void *d_rec = nullptr;  // single-step record (vpm_plan_step)
   // rollout-kernel timing
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // start/stop pairs
@@ -677,20 +676,16 @@ int vpm_plan_step(vpm_plan *p, const double *x, double u, int integrate, const d
   // a page-locked record buffer is written by the kernels themselves (unified
   // addressing: the pinned host page is device-accessible), saving the queued copy
   // and its stream slot; pageable buffers go through the device record and a copy
+  // (queried on every call: a cached answer could outlive the caller's buffer)
   bool direct = false;
   if (h_record) {
-    if (h_record != p->rec_host) {
-      cudaPointerAttributes at;
-      p->rec_host = h_record;
-      p->rec_dev = nullptr;
-      if (cudaPointerGetAttributes(&at, h_record) == cudaSuccess && at.type == cudaMemoryTypeHost)
-        p->rec_dev = at.devicePointer;
-      cudaGetLastError();  // a pageable pointer is not an error here
-    }
-    if (p->rec_dev) {
-      r = (StepRecord *)p->rec_dev;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h_record) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+        at.devicePointer) {
+      r = (StepRecord *)at.devicePointer;
       direct = true;
     }
+    cudaGetLastError();  // a pageable pointer is not an error here
   }
   Args a = base_args(p);
   a.use_x0v = 1;
